@@ -1,0 +1,172 @@
+/*
+ * lcma.h -- C ABI of the B200-native LCMA GEMM library (liblcma.so).
+ *
+ * The library computes C = A * B (Eq. 1) either with a
+ * classical tcgen05 GEMM or through a Lower-Complexity Matrix Multiplication
+ * Algorithm <m,k,n,R,U,V,W>: Combine A (Eq. 3),
+ * Combine B (Eq. 4), R sub-GEMMs H_r = At_r * Bt_r (Eq. 5,
+ * P:630-634) and Combine H (Eq. 6), organised by the paper's
+ * group-parallel fusion (Alg. 2; Split-Group P:362-387;
+ * Cache-Aware P:391-396) and chosen by the Decision Module.
+ * "P:n" = /root/reference/PAPER.md line n, "S:n" = SPEC.md line n.
+ *
+ * Conventions (all entry points):
+ *  - Shapes are (M, N, K); A is M x K, B is K x N (b_layout 0, the paper's
+ *    layout) or N x K (b_layout 1, nn.Linear weight), C is M x N; all
+ *    row-major with the leading dimension equal to the row length.
+ *  - A, B, Bt, C and the workspace are DEVICE pointers owned by the caller.
+ *    They must be 16-byte aligned and row lengths must be multiples of
+ *    16 bytes (TMA), else LCMA_ERR_MISALIGNED.  There is no CPU fallback and
+ *    no silent copy.
+ *  - The plan owns host metadata only; it is immutable after creation and
+ *    may be shared across threads.  lcma_free(NULL) is a no-op.
+ *  - lcma_gemm* only enqueue work on `cuda_stream` (a cudaStream_t; NULL =
+ *    legacy default stream): no allocation, no host synchronisation, so they
+ *    are CUDA-graph capturable.  Launch failures return LCMA_ERR_CUDA with
+ *    the CUDA error string in lcma_last_error(); asynchronous faults surface
+ *    at the caller's next synchronisation.
+ *  - The workspace must be zero-filled once before its first use (the
+ *    library keeps its split-group flags at zero between calls).
+ *  - Results are bitwise deterministic for a fixed plan: no floating-point
+ *    atomics; split groups merge in a fixed order (reading 10).
+ */
+#ifndef LCMA_H_
+#define LCMA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LCMA_OK = 0,
+    LCMA_ERR_INVALID_VALUE = 1,  /* bad shape/enum/pointer, aliasing C with inputs */
+    LCMA_ERR_NOT_SUPPORTED = 2,  /* combination not built (e.g. dtype x algo)       */
+    LCMA_ERR_MISALIGNED = 3,     /* TMA 16-byte rules violated                      */
+    LCMA_ERR_SCHEME_INVALID = 4, /* Brent identity fails; see lcma_last_error */
+    LCMA_ERR_COEFF_RANGE = 5,    /* coefficient outside {-1,0,1}      */
+    LCMA_ERR_PARSE = 6,          /* scheme file syntax error, line in message */
+    LCMA_ERR_WORKSPACE = 7,      /* workspace too small                             */
+    LCMA_ERR_CUDA = 8            /* CUDA runtime/driver error                       */
+} lcma_status;
+
+typedef enum {
+    LCMA_BF16 = 0,   /* bf16 storage, bf16 MMA, fp32 accumulation                  */
+    LCMA_FP16 = 1,   /* fp16 storage, fp16 MMA, fp32 accumulation                  */
+    LCMA_TF32 = 2,   /* fp32 storage, tf32 MMA (RN-away rounding of combined terms) */
+    LCMA_FP32 = 3    /* fp32 storage, true fp32 SIMT arithmetic                     */
+} lcma_dtype;
+
+typedef enum {
+    LCMA_ALGO_AUTO = 0,        /* Decision Module picks               */
+    LCMA_ALGO_CLASSICAL = 1,   /* single tcgen05 GEMM (the no-LCMA reference)     */
+    LCMA_ALGO_STRASSEN = 2,    /* <2,2,2;7>, depth 1                      */
+    LCMA_ALGO_STRASSEN2 = 3,   /* <4,4,4;49> = Strassen composed twice, depth 2 */
+    LCMA_ALGO_LADERMAN = 4,    /* <3,3,3;23>                              */
+    LCMA_ALGO_SCHEME = 5       /* scheme registered from a file (scheme_id)       */
+} lcma_algo;
+
+typedef enum {
+    LCMA_VARIANT_AUTO = 0,
+    LCMA_VARIANT_UNFUSED = 1,  /* Algorithm 1: At, Bt, H materialised     */
+    LCMA_VARIANT_FUSED_H = 2,  /* Algorithm 2: At/Bt materialised by group-parallel
+                                  combines, GEMM + Combine H fused       */
+    LCMA_VARIANT_PRODUCER = 3  /* Combine A/B in the GEMM producer, Combine H fused  */
+} lcma_variant;
+
+typedef struct lcma_plan_s* lcma_plan_t;
+
+/* Hardware triple of P:171-175: FLOPS_x (GEMM stage), FLOPS_+ (combine adds),
+ * beta (off-chip bandwidth in ELEMENTS/s of the dtype), worker count. */
+typedef struct {
+    double flops_mul;
+    double flops_add;
+    double beta_elems;
+    int32_t workers;
+} lcma_hw_profile;
+
+typedef struct {
+    int64_t M, N, K;
+    lcma_dtype dtype;
+    lcma_dtype out_dtype;     /* C element type: same as dtype, or LCMA_FP32      */
+    lcma_algo algo;
+    int32_t scheme_id;        /* for LCMA_ALGO_SCHEME                              */
+    int32_t b_layout;         /* 0: B is K x N (paper), 1: B is N x K              */
+    int32_t b_static;         /* 1: lcma_gemm_precombined will be used     */
+    int32_t variant;          /* lcma_variant                                      */
+    int32_t schedule;         /* 0 auto, 1 lockstep rounds + split tail (cache-aware),
+                                 2 paper's contiguous split-group order           */
+    int32_t num_ctas;         /* 0 = one per SM                                    */
+    const lcma_hw_profile* hw;/* NULL -> built-in B200 profile                     */
+} lcma_plan_desc;
+
+typedef struct {
+    lcma_algo algo;           /* resolved algorithm                               */
+    int32_t variant;          /* resolved lcma_variant                            */
+    int32_t m, k, n, R, depth;
+    char scheme[64];
+    int64_t Mb, Nb, Kb;       /* padded block extents (>= ceil(M/m) etc.)  */
+    int32_t BM, BN, BK;
+    int32_t groups, tiles, ctas, waves, group_waves, split_groups;
+    double t_pred_classical, t_pred_choice, speedup_pred;  /* seconds, model      */
+    int32_t memory_bound;     /* Eq. stdgemm held                          */
+    int32_t lcma_condition;   /* Eq. lcma_condition holds                  */
+    int32_t fused_condition;  /* Eq. fused_condition holds                 */
+    size_t workspace_bytes, btilde_bytes;
+} lcma_plan_info;
+
+/* Create a plan for C = A*B of shape (M,N,K).  out: new plan on LCMA_OK. */
+lcma_status lcma_plan(int64_t M, int64_t N, int64_t K, lcma_dtype dtype,
+                      lcma_algo algo, lcma_plan_t* out);
+lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out);
+void lcma_free(lcma_plan_t plan);
+lcma_status lcma_plan_get_info(lcma_plan_t plan, lcma_plan_info* out);
+lcma_status lcma_workspace_size(lcma_plan_t plan, size_t* bytes);
+lcma_status lcma_btilde_size(lcma_plan_t plan, size_t* bytes);
+
+/* C = A*B on the device.  workspace: >= lcma_workspace_size bytes (zeroed
+ * before first use).  Number of kernels launched is reported by
+ * lcma_last_launch_count(). */
+lcma_status lcma_gemm(lcma_plan_t plan, const void* A, const void* B, void* C,
+                      void* workspace, size_t workspace_bytes, void* cuda_stream);
+
+/* Offline Combine B for static weights: Bt = group-combined
+ * B for this plan's scheme and extents (lcma_btilde_size bytes).  Bt is bound
+ * to the plan's (N, K, dtype, scheme, extents, b_layout); lcma_gemm_precombined
+ * trusts the caller to pass a matching Bt. */
+lcma_status lcma_precombine_b(lcma_plan_t plan, const void* B, void* Bt, void* cuda_stream);
+lcma_status lcma_gemm_precombined(lcma_plan_t plan, const void* A, const void* Bt, void* C,
+                                  void* workspace, size_t workspace_bytes, void* cuda_stream);
+
+/* Decision Module only (host, no device): fills algo/scheme/t_pred_* and
+ * the Eq. flags.  fused: 1 -> Eq. fused_condition model. */
+lcma_status lcma_decide(int64_t M, int64_t N, int64_t K, lcma_dtype dtype,
+                        const lcma_hw_profile* hw, int32_t fused, lcma_plan_info* out);
+
+/* Scheme registry.  Built-in ids: 0 classical(1,1,1), 1 Strassen, 2 Strassen^2,
+ * 3 Laderman.  Registration validates the Brent identity. */
+lcma_status lcma_scheme_register_file(const char* path, int32_t* scheme_id);
+lcma_status lcma_scheme_register(int32_t m, int32_t k, int32_t n, int32_t R,
+                                 const int8_t* U, const int8_t* V, const int8_t* W,
+                                 const char* name, int32_t* scheme_id);
+/* mknR[4] <- (m,k,n,R); U/V/W (may be NULL) <- R*m*k, R*k*n, R*m*n int8. */
+lcma_status lcma_scheme_get(int32_t scheme_id, int32_t* mknR, int8_t* U, int8_t* V, int8_t* W);
+
+/* Split-group schedule of a plan (host view of the device enumeration):
+ * for CTA `cta`, writes up to `cap` units as (group, r_begin, r_end, role)
+ * int32 quadruples (role 0 whole group, 1 owner segment, 2 contributing
+ * segment) and returns the count in *n. */
+lcma_status lcma_plan_schedule(lcma_plan_t plan, int32_t cta, int32_t* units, int32_t cap,
+                               int32_t* n);
+
+/* Thread-local message for the last error on this thread ("" if none). */
+const char* lcma_last_error(void);
+/* Number of kernels the last lcma_gemm* call on this thread enqueued. */
+int32_t lcma_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LCMA_H_ */

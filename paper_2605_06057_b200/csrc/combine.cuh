@@ -1,0 +1,273 @@
+// combine.cuh -- group-parallel combine kernels (Algorithm 2 stages 1-2,
+// P:300-320, and the group Combine H of the unfused path, P:95-100 reordered
+// per P:355-358).  Each thread owns one relative coordinate (x, y) of the
+// block grid, loads the m*k (k*n) source elements A_{i,l}[x,y] exactly once
+// and emits every At_r[x,y] of the group: reads of the source = 1x, writes =
+// R x (Table "cost_model" memory column MK(1 + R/mk)).  HBM-bound.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace lcma {
+
+constexpr int kCombMaxR = 128;
+constexpr int kCombMaxPQ = 32;
+
+enum ElemType : int { ELEM_BF16 = 0, ELEM_FP16 = 1, ELEM_FP32 = 2 };
+
+struct CombineParams {
+    const void* src;          // rows x cols row-major
+    void* dst;                // [R][E0][E1] row-major
+    long long rows, cols;     // true source extents (zero padding beyond)
+    long long E0, E1;         // block extents (multiples of 8 along E1)
+    int P, Q;                 // source block grid
+    int R;
+    int elem;                 // ElemType
+    int round_tf32;           // fp32 outputs rounded RN-away to tf32
+    int8_t coef[kCombMaxR * kCombMaxPQ];   // coef[r][p*Q + q]
+};
+
+template <int VEC>
+__device__ __forceinline__ void load_vec(const CombineParams& p, long long r, long long c, float* v) {
+    if (r >= p.rows || c >= p.cols) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) v[e] = 0.f;
+        return;
+    }
+    const long long off = r * p.cols + c;
+    if (p.elem == ELEM_FP32) {
+        const float4* s = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.src) + off);
+#pragma unroll
+        for (int e = 0; e < VEC; e += 4) {
+            float4 t = __ldg(s + e / 4);
+            v[e] = t.x; v[e + 1] = t.y; v[e + 2] = t.z; v[e + 3] = t.w;
+        }
+    } else {
+        const uint16_t* s = reinterpret_cast<const uint16_t*>(p.src) + off;
+        uint32_t w[VEC / 2];
+        if (VEC == 8) {
+            uint4 t = __ldg(reinterpret_cast<const uint4*>(s));
+            w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+        } else {
+            uint2 t = __ldg(reinterpret_cast<const uint2*>(s));
+            w[0] = t.x; w[1] = t.y;
+        }
+#pragma unroll
+        for (int h = 0; h < VEC / 2; ++h) {
+            if (p.elem == ELEM_BF16) {
+                __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w[h]);
+                float2 f = __bfloat1622float2(b);
+                v[2 * h] = f.x; v[2 * h + 1] = f.y;
+            } else {
+                __half2 b = *reinterpret_cast<__half2*>(&w[h]);
+                float2 f = __half22float2(b);
+                v[2 * h] = f.x; v[2 * h + 1] = f.y;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ float round_tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+template <int VEC>
+__device__ __forceinline__ void store_vec(const CombineParams& p, long long off, const float* v) {
+    if (p.elem == ELEM_FP32) {
+        float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.dst) + off);
+#pragma unroll
+        for (int e = 0; e < VEC; e += 4) {
+            float a = v[e], b = v[e + 1], c = v[e + 2], dd = v[e + 3];
+            if (p.round_tf32) {
+                a = round_tf32_rna(a); b = round_tf32_rna(b);
+                c = round_tf32_rna(c); dd = round_tf32_rna(dd);
+            }
+            d[e / 4] = make_float4(a, b, c, dd);
+        }
+    } else {
+        uint32_t w[VEC / 2];
+#pragma unroll
+        for (int h = 0; h < VEC / 2; ++h) {
+            if (p.elem == ELEM_BF16) {
+                __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+                w[h] = *reinterpret_cast<uint32_t*>(&b);
+            } else {
+                __half2 b = __floats2half2_rn(v[2 * h], v[2 * h + 1]);
+                w[h] = *reinterpret_cast<uint32_t*>(&b);
+            }
+        }
+        uint16_t* d = reinterpret_cast<uint16_t*>(p.dst) + off;
+        if (VEC == 8)
+            *reinterpret_cast<uint4*>(d) = make_uint4(w[0], w[1], w[2], w[3]);
+        else
+            *reinterpret_cast<uint2*>(d) = make_uint2(w[0], w[1]);
+    }
+}
+
+// Group Combine (Alg. 2 lines 2-9 / 11-18): out_r[e0][e1] =
+// sum_{p,q} coef[r][p][q] * src[p*E0 + e0][q*E1 + e1], fp32 sum, one rounding.
+template <int VEC, int PQ>
+__global__ void __launch_bounds__(256) group_combine_kernel(const __grid_constant__ CombineParams p) {
+    const long long nvec = p.E0 * (p.E1 / VEC);
+    const long long per_r = p.E0 * p.E1;
+    for (long long vi = blockIdx.x * (long long)blockDim.x + threadIdx.x; vi < nvec;
+         vi += (long long)gridDim.x * blockDim.x) {
+        const long long e0 = vi / (p.E1 / VEC);
+        const long long e1 = (vi - e0 * (p.E1 / VEC)) * VEC;
+        float src[PQ][VEC];
+#pragma unroll
+        for (int pq = 0; pq < PQ; ++pq) {
+            const int pi = pq / p.Q, qi = pq - (pq / p.Q) * p.Q;
+            load_vec<VEC>(p, pi * p.E0 + e0, qi * p.E1 + e1, src[pq]);
+        }
+        for (int r = 0; r < p.R; ++r) {
+            float acc[VEC];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
+#pragma unroll
+            for (int pq = 0; pq < PQ; ++pq) {
+                const int c = p.coef[r * PQ + pq];
+                if (c == 1) {
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) acc[e] += src[pq][e];
+                } else if (c == -1) {
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) acc[e] -= src[pq][e];
+                }
+            }
+            store_vec<VEC>(p, (long long)r * per_r + e0 * p.E1 + e1, acc);
+        }
+    }
+}
+
+// Group Combine H for the unfused path: each thread owns H_r[x][z..z+3] for
+// all r (read once) and produces C_ij[x][z..z+3] for all (i,j).
+struct CombineHParams {
+    const float* H;           // [R][Mb][Nb]
+    void* C;                  // M x N, ldc
+    long long M, N, Mb, Nb, ldc;
+    int m, n, R;
+    int out_type;             // 0 bf16, 1 fp16, 2 fp32
+    int8_t Wc[kCombMaxR * kCombMaxPQ];   // W[r][i*n + j]
+};
+
+template <int MN>
+__global__ void __launch_bounds__(256) group_combine_h_kernel(const __grid_constant__ CombineHParams p) {
+    const long long nvec = p.Mb * (p.Nb / 4);
+    for (long long vi = blockIdx.x * (long long)blockDim.x + threadIdx.x; vi < nvec;
+         vi += (long long)gridDim.x * blockDim.x) {
+        const long long x = vi / (p.Nb / 4);
+        const long long z = (vi - x * (p.Nb / 4)) * 4;
+        float acc[MN][4];
+#pragma unroll
+        for (int ij = 0; ij < MN; ++ij)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[ij][e] = 0.f;
+        for (int r = 0; r < p.R; ++r) {
+            const float4 h = __ldg(reinterpret_cast<const float4*>(p.H + ((long long)r * p.Mb + x) * p.Nb + z));
+#pragma unroll
+            for (int ij = 0; ij < MN; ++ij) {
+                const int w = p.Wc[r * MN + ij];
+                if (w) {
+                    const float s = (float)w;
+                    acc[ij][0] += s * h.x; acc[ij][1] += s * h.y;
+                    acc[ij][2] += s * h.z; acc[ij][3] += s * h.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int ij = 0; ij < MN; ++ij) {
+            const int i = ij / p.n, j = ij % p.n;
+            const long long row = i * p.Mb + x, col = j * p.Nb + z;
+            if (row >= p.M || col >= p.N) continue;
+            if (p.out_type == 2) {
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.C) + row * p.ldc + col) =
+                    make_float4(acc[ij][0], acc[ij][1], acc[ij][2], acc[ij][3]);
+            } else {
+                uint32_t w2[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (p.out_type == 0) {
+                        __nv_bfloat162 b = __floats2bfloat162_rn(acc[ij][2 * h], acc[ij][2 * h + 1]);
+                        w2[h] = *reinterpret_cast<uint32_t*>(&b);
+                    } else {
+                        __half2 b = __floats2half2_rn(acc[ij][2 * h], acc[ij][2 * h + 1]);
+                        w2[h] = *reinterpret_cast<uint32_t*>(&b);
+                    }
+                }
+                *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.C) + row * p.ldc + col) =
+                    make_uint2(w2[0], w2[1]);
+            }
+        }
+    }
+}
+
+// True-fp32 batched SIMT GEMM (dtype LCMA_FP32): H_r = At_r * Bt_r with
+// At_r = A + r*sAr (rows x K, lda), Bt_r = B + r*sBr; B is K x N (ldb) or,
+// with b_kmajor, N x K.  128 x 128 output tile per 256-thread block, 8 x 8
+// per thread, BK = 8 staged through shared memory.
+struct SimtParams {
+    const float* A; const float* B; float* H;
+    long long Mr, Nr, Kr;         // per-product extents
+    long long lda, ldb, ldh;
+    long long sAr, sBr, sHr;      // per-r strides (elements)
+    int b_kmajor;
+};
+
+__global__ void __launch_bounds__(256) simt_sgemm_batched_kernel(const __grid_constant__ SimtParams p) {
+    __shared__ float sA[8][128 + 4];
+    __shared__ float sB[8][128 + 4];
+    const int r = blockIdx.z;
+    const long long m0 = (long long)blockIdx.y * 128, n0 = (long long)blockIdx.x * 128;
+    const float* A = p.A + r * p.sAr;
+    const float* B = p.B + r * p.sBr;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (long long k0 = 0; k0 < p.Kr; k0 += 8) {
+        for (int t = threadIdx.x; t < 8 * 128; t += 256) {
+            const int kk = t % 8, mm = t / 8;
+            const long long gm = m0 + mm, gk = k0 + kk;
+            sA[kk][mm] = (gm < p.Mr && gk < p.Kr) ? A[gm * p.lda + gk] : 0.f;
+            const int nn = p.b_kmajor ? t / 8 : t % 128;
+            const int kb = p.b_kmajor ? t % 8 : t / 128;
+            const long long gn = n0 + nn, gk2 = k0 + kb;
+            float bv = 0.f;
+            if (gn < p.Nr && gk2 < p.Kr) bv = p.b_kmajor ? B[gn * p.ldb + gk2] : B[gk2 * p.ldb + gn];
+            sB[kb][nn] = bv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            float a[8], b[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = sA[kk][ty * 8 + i];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = sB[kk][tx * 8 + j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    float* Hr = p.H + r * p.sHr;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const long long gm = m0 + ty * 8 + i;
+        if (gm >= p.Mr) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const long long gn = n0 + tx * 8 + j;
+            if (gn < p.Nr) Hr[gm * p.ldh + gn] = acc[i][j];
+        }
+    }
+}
+
+}  // namespace lcma

@@ -1,0 +1,114 @@
+// decision.cpp -- the paper's analytical cost model (Sec. III-C):
+// hardware triple (FLOPS_x, FLOPS_+, beta), Eq. stdgemm early exit, Table
+// "cost_model" per-stage FLOPs / memory, per-stage time = compute time if the
+// stage's arithmetic intensity exceeds the device ratio, else memory time
+// (P:236-237), stages summed without overlap, argmin with classical fallback.
+#include "decision.h"
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+namespace lcma {
+
+static double cdiv(double a, double b) { return std::ceil(a / b); }
+
+double gemm_intensity(double M, double N, double K) {
+    return 2.0 * M * N * K / (M * K + N * K + M * N);
+}
+
+double estimate_time_std(double M, double N, double K, const Profile& hw) {
+    return 2.0 * M * N * K / hw.flops_mul;
+}
+
+static StageCost stage(double flops, double mem, double thr, double beta) {
+    StageCost c;
+    c.flops = flops;
+    c.mem = mem;
+    // compute-bound iff flops/mem > FLOPS/beta (strict)
+    c.compute_bound = mem > 0 && (flops / mem) > (thr / beta);
+    c.time = c.compute_bound ? flops / thr : mem / beta;
+    return c;
+}
+
+void stage_costs(const Scheme& s, double M, double N, double K, const Profile& hw, bool fused,
+                 bool b_static, StageCost out[4]) {
+    const double R = s.R;
+    const double Mq = cdiv(M, s.m), Kq = cdiv(K, s.k), Nq = cdiv(N, s.n);
+    // Combine A: (||U||_0 - R) (M/m)(K/k) adds, MK + R (M/m)(K/k) elements
+    out[0] = stage((s.nnzU() - R) * Mq * Kq, M * K + R * Mq * Kq, hw.flops_add, hw.beta);
+    // Combine B; offline for static weights
+    if (b_static) {
+        out[1] = StageCost{0.0, 0.0, 0.0, false};
+    } else {
+        out[1] = stage((s.nnzV() - R) * Kq * Nq, N * K + R * Kq * Nq, hw.flops_add, hw.beta);
+    }
+    // GEMM stage: 2R (M/m)(N/n)(K/k) flops; R(MK/mk + NK/nk + MN/mn) elements,
+    // fused: the R H writes become a single C write
+    const double gm = R * (Mq * Kq + Kq * Nq) + (fused ? M * N : R * Mq * Nq);
+    out[2] = stage(2.0 * R * Mq * Nq * Kq, gm, hw.flops_mul, hw.beta);
+    // Combine H: (||W||_0 - mn)(M/m)(N/n) adds; MN(1 + R/mn), fused: MN
+    const double hm = fused ? M * N : M * N + R * Mq * Nq;
+    out[3] = stage((s.nnzW() - (double)s.m * s.n) * Mq * Nq, hm, hw.flops_add, hw.beta);
+}
+
+double estimate_time(const Scheme& s, double M, double N, double K, const Profile& hw, bool fused,
+                     bool b_static) {
+    StageCost c[4];
+    stage_costs(s, M, N, K, hw, fused, b_static, c);
+    return c[0].time + c[1].time + c[2].time + c[3].time;
+}
+
+double condition_lhs(const Scheme& s, double M, double N, double K, bool fused) {
+    const double m = s.m, k = s.k, n = s.n, R = s.R;
+    const double num = 2.0 * M * N * K * (1.0 - R / (m * n * k));
+    const double den = M * K * (1.0 + R / (m * k)) + N * K * (1.0 + R / (n * k)) +
+                       M * N * (fused ? 1.0 : 1.0 + R / (m * n));
+    return num / den;
+}
+
+DecisionResult decide(const std::vector<int>& ids, double M, double N, double K, const Profile& hw,
+                      bool fused, bool b_static) {
+    DecisionResult d;
+    d.scheme_id = SCHEME_CLASSICAL;
+    d.t_std = estimate_time_std(M, N, K, hw);
+    d.t_choice = d.t_std;
+    d.memory_bound = gemm_intensity(M, N, K) <= hw.flops_mul / hw.beta;   // Eq. stdgemm, "<="
+    if (d.memory_bound) return d;
+    for (int id : ids) {
+        const Scheme* s = scheme_get(id);
+        if (!s || s->R >= s->m * s->k * s->n) continue;
+        const double t = estimate_time(*s, M, N, K, hw, fused, b_static);
+        d.candidates.emplace_back(id, t);
+        if (t < d.t_choice) {
+            d.t_choice = t;
+            d.scheme_id = id;
+        }
+    }
+    return d;
+}
+
+Profile default_profile(int dtype) {
+    // Measured on this pool's B200s (MEASURED_PEAKS.json): bf16 GEMM sustained
+    // 1.39 PFLOP/s under the power cap, HBM copy 6.55 TB/s; FLOPS_+ = fp32
+    // FADD issue rate 148 SMs x 128 lanes x ~1.3 GHz sustained.
+    Profile p;
+    const double bytes = (dtype == 0 || dtype == 1) ? 2.0 : 4.0;
+    p.flops_mul = dtype <= 1 ? 1.39e15 : (dtype == 2 ? 0.69e15 : 60e12);
+    p.flops_add = 148.0 * 128.0 * 1.3e9;
+    p.beta = 6.55e12 / bytes;
+    if (const char* env = std::getenv("LCMA_PROFILE")) {
+        const char* keys[3] = {"flops_mul=", "flops_add=", "beta_elems="};
+        double* dst[3] = {&p.flops_mul, &p.flops_add, &p.beta};
+        for (int i = 0; i < 3; ++i) {
+            const char* f = std::strstr(env, keys[i]);
+            if (f) {
+                double v = std::atof(f + std::strlen(keys[i]));
+                if (v > 0) *dst[i] = v;
+            }
+        }
+    }
+    return p;
+}
+
+}  // namespace lcma

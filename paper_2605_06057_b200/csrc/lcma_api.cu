@@ -1,0 +1,698 @@
+// lcma_api.cu -- C ABI of liblcma.so (see include/lcma.h): plan creation
+// (Decision Module, block extents, split-group schedule, workspace layout),
+// TMA descriptor encoding and kernel launches.  No CPU fallback: every step
+// of C = A*B runs in the kernels of umma_gemm.cuh / combine.cuh.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <string>
+
+#include "../../include/lcma.h"
+#include "combine.cuh"
+#include "decision.h"
+#include "schemes.h"
+#include "umma_gemm.cuh"
+
+using namespace lcma;
+
+namespace {
+
+thread_local std::string t_err;
+thread_local int t_launches = 0;
+
+lcma_status fail(lcma_status st, const std::string& msg) {
+    t_err = msg;
+    return st;
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t roundup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int elem_bytes(lcma_dtype d) { return (d == LCMA_BF16 || d == LCMA_FP16) ? 2 : 4; }
+
+int device_sm_count() {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 148; }
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+        cudaGetLastError();
+        return 148;
+    }
+    return sms;
+}
+
+}  // namespace
+
+struct lcma_plan_s {
+    lcma_plan_desc d;
+    Profile hw;
+    int scheme_id;
+    Scheme sch;
+    lcma_algo algo;
+    int variant;
+    int64_t Mb, Nb, Kb;
+    int BK, e;
+    int nX, nZ, G, nK;
+    int ctas, q, tail_c, swz;
+    size_t off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
+    lcma_plan_info info;
+};
+
+// ---------------------------------------------------------------- schedule
+namespace {
+
+struct HostUnit { int g, r0, r1, role; };
+
+// Mirror of the device UnitIter (umma_gemm.cuh).
+std::vector<HostUnit> host_units(const lcma_plan_s* p, int w) {
+    std::vector<HostUnit> out;
+    const int R = p->sch.R;
+    for (int i = 0; i < p->q; ++i) out.push_back({i * p->ctas + w, 0, R, ROLE_WHOLE});
+    const long long Tt = (long long)(p->G - p->q * p->ctas) * R;
+    long long t = std::min<long long>((long long)w * p->tail_c, Tt);
+    long long t_end = std::min<long long>(t + p->tail_c, Tt);
+    while (t < t_end) {
+        long long gl = t / R;
+        int r0 = (int)(t - gl * R);
+        long long stop = std::min<long long>((gl + 1) * R, t_end);
+        int r1 = (int)(stop - gl * R);
+        int role = (r0 == 0 && r1 == R) ? ROLE_WHOLE : (r0 == 0 ? ROLE_OWNER : ROLE_CONTRIB);
+        out.push_back({p->q * p->ctas + (int)gl, r0, r1, role});
+        t = stop;
+    }
+    return out;
+}
+
+void make_schedule(lcma_plan_s* p, int mode) {
+    const int R = p->sch.R;
+    const int W = p->ctas;
+    if (mode == 2) {
+        p->q = 0;                              // paper: contiguous split-group chunks
+    } else {
+        p->q = p->G / W;                       // lockstep rounds (cache-aware)
+    }
+    const long long Tt = (long long)(p->G - p->q * W) * R;
+    p->tail_c = Tt > 0 ? (int)cdiv(Tt, W) : 1;
+    p->swz = 16;
+    p->info.groups = p->G;
+    p->info.tiles = (int)std::min<long long>((long long)p->G * R, INT32_MAX);
+    p->info.ctas = W;
+    p->info.waves = p->q * R + (Tt > 0 ? p->tail_c : 0);
+    p->info.group_waves = (int)cdiv(p->G, W) * R;
+    int splits = 0;
+    for (long long gl = 0; gl < p->G - p->q * W; ++gl) {
+        long long a = gl * R, b = gl * R + R - 1;
+        if (a / p->tail_c != b / p->tail_c) ++splits;
+    }
+    p->info.split_groups = splits;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- planning
+extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out) {
+    t_err.clear();
+    if (!desc || !out) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    *out = nullptr;
+    const lcma_plan_desc& d = *desc;
+    if (d.M < 1 || d.N < 1 || d.K < 1) return fail(LCMA_ERR_INVALID_VALUE, "M, N, K must be >= 1");
+    if (d.dtype < LCMA_BF16 || d.dtype > LCMA_FP32) return fail(LCMA_ERR_INVALID_VALUE, "bad dtype");
+    lcma_dtype od = d.out_dtype;
+    if (od != d.dtype && od != LCMA_FP32) return fail(LCMA_ERR_NOT_SUPPORTED, "out_dtype must equal dtype or be FP32");
+    if (d.dtype == LCMA_TF32 && od != LCMA_FP32 && od != LCMA_TF32)
+        return fail(LCMA_ERR_NOT_SUPPORTED, "tf32 output is fp32");
+    if (d.b_layout != 0 && d.b_layout != 1) return fail(LCMA_ERR_INVALID_VALUE, "b_layout must be 0 or 1");
+    if (d.algo < LCMA_ALGO_AUTO || d.algo > LCMA_ALGO_SCHEME) return fail(LCMA_ERR_INVALID_VALUE, "bad algo");
+    if (d.variant < 0 || d.variant > 3) return fail(LCMA_ERR_INVALID_VALUE, "bad variant");
+    const int e = elem_bytes(d.dtype);
+    if ((d.K * e) % 16 != 0 || (d.N * e) % 16 != 0)
+        return fail(LCMA_ERR_MISALIGNED, "K and N row lengths must be multiples of 16 bytes (TMA)");
+
+    auto* p = new lcma_plan_s();
+    p->d = d;
+    p->e = e;
+    p->hw = d.hw ? Profile{d.hw->flops_mul, d.hw->flops_add, d.hw->beta_elems}
+                 : default_profile((int)d.dtype);
+    if (!(p->hw.flops_mul > 0 && p->hw.flops_add > 0 && p->hw.beta > 0)) {
+        delete p;
+        return fail(LCMA_ERR_INVALID_VALUE, "hardware profile entries must be > 0");
+    }
+    std::memset(&p->info, 0, sizeof(p->info));
+
+    // ---- Decision Module; reported even when algo is forced
+    const bool fused_model = d.variant != LCMA_VARIANT_UNFUSED && d.dtype != LCMA_FP32;
+    std::vector<int> cands = {SCHEME_STRASSEN, SCHEME_STRASSEN2, SCHEME_LADERMAN};
+    DecisionResult dec = decide(cands, (double)d.M, (double)d.N, (double)d.K, p->hw, fused_model,
+                                d.b_static != 0);
+    switch (d.algo) {
+        case LCMA_ALGO_AUTO: p->scheme_id = dec.scheme_id; break;
+        case LCMA_ALGO_CLASSICAL: p->scheme_id = SCHEME_CLASSICAL; break;
+        case LCMA_ALGO_STRASSEN: p->scheme_id = SCHEME_STRASSEN; break;
+        case LCMA_ALGO_STRASSEN2: p->scheme_id = SCHEME_STRASSEN2; break;
+        case LCMA_ALGO_LADERMAN: p->scheme_id = SCHEME_LADERMAN; break;
+        case LCMA_ALGO_SCHEME: p->scheme_id = d.scheme_id; break;
+    }
+    const Scheme* s = scheme_get(p->scheme_id);
+    if (!s) {
+        delete p;
+        return fail(LCMA_ERR_INVALID_VALUE, "unknown scheme id");
+    }
+    p->sch = *s;
+    const bool classical = (p->scheme_id == SCHEME_CLASSICAL);
+    p->algo = classical ? LCMA_ALGO_CLASSICAL
+                        : (p->scheme_id == SCHEME_STRASSEN ? LCMA_ALGO_STRASSEN
+                           : p->scheme_id == SCHEME_STRASSEN2 ? LCMA_ALGO_STRASSEN2
+                           : p->scheme_id == SCHEME_LADERMAN ? LCMA_ALGO_LADERMAN
+                                                             : LCMA_ALGO_SCHEME);
+    // ---- variant
+    int variant = d.variant;
+    if (classical) variant = 0;
+    else if (d.dtype == LCMA_FP32) {
+        if (variant == LCMA_VARIANT_AUTO) variant = LCMA_VARIANT_UNFUSED;
+        if (variant != LCMA_VARIANT_UNFUSED) {
+            delete p;
+            return fail(LCMA_ERR_NOT_SUPPORTED, "fp32 (SIMT) LCMA runs the unfused variant only");
+        }
+    } else {
+        if (variant == LCMA_VARIANT_AUTO) variant = LCMA_VARIANT_FUSED_H;
+        if (variant == LCMA_VARIANT_PRODUCER) {
+            delete p;
+            return fail(LCMA_ERR_NOT_SUPPORTED, "producer-fused variant not built yet");
+        }
+    }
+    p->variant = variant;
+
+    // ---- blocking (P:612 ceil extents, tile-rounded: DESIGN.md reading 6)
+    const Scheme& S = p->sch;
+    if (d.dtype == LCMA_FP32) {
+        p->BK = 8;
+        p->Mb = classical ? d.M : roundup(cdiv(d.M, S.m), 8);
+        p->Nb = classical ? d.N : roundup(cdiv(d.N, S.n), 8);
+        p->Kb = classical ? d.K : roundup(cdiv(d.K, S.k), 8);
+        p->nX = p->nZ = p->nK = 0;
+        p->G = 0;
+        p->ctas = 0;
+    } else {
+        p->BK = 128 / e;
+        if (classical) {
+            p->nX = (int)cdiv(d.M, kBM);
+            p->nZ = (int)cdiv(d.N, kBN);
+            p->nK = (int)cdiv(d.K, p->BK);
+            p->Mb = (int64_t)p->nX * kBM;
+            p->Nb = (int64_t)p->nZ * kBN;
+            p->Kb = (int64_t)p->nK * p->BK;
+        } else {
+            p->Mb = roundup(cdiv(d.M, S.m), kBM);
+            p->Nb = roundup(cdiv(d.N, S.n), kBN);
+            p->Kb = roundup(cdiv(d.K, S.k), p->BK);
+            p->nX = (int)(p->Mb / kBM);
+            p->nZ = (int)(p->Nb / kBN);
+            p->nK = (int)(p->Kb / p->BK);
+        }
+        if ((long long)p->nX * p->nZ > INT32_MAX / 2 || S.R * p->Mb > INT32_MAX ||
+            S.R * p->Kb > INT32_MAX || S.R * p->Nb > INT32_MAX) {
+            delete p;
+            return fail(LCMA_ERR_NOT_SUPPORTED, "problem too large for 32-bit tile coordinates");
+        }
+        p->G = p->nX * p->nZ;
+        const int sms = device_sm_count();
+        p->ctas = d.num_ctas > 0 ? std::min(d.num_ctas, sms) : sms;
+        make_schedule(p, d.schedule == 2 ? 2 : 1);
+    }
+
+    // ---- workspace layout
+    size_t off = 0;
+    p->off_P = p->off_flags = p->off_At = p->off_Bt = p->off_H = 0;
+    const int mn = S.m * S.n;
+    if (!classical) {
+        if (d.dtype != LCMA_FP32 && variant == LCMA_VARIANT_FUSED_H) {
+            p->off_P = off;
+            off = align256(off + (size_t)2 * p->ctas * mn * kBM * kBN * sizeof(float));
+            p->off_flags = off;
+            off = align256(off + (size_t)p->ctas * sizeof(int));
+        }
+        p->off_At = off;
+        off = align256(off + (size_t)S.R * p->Mb * p->Kb * e);
+        p->off_Bt = off;
+        off = align256(off + (size_t)S.R * p->Kb * p->Nb * e);
+        if (variant == LCMA_VARIANT_UNFUSED) {
+            p->off_H = off;
+            off = align256(off + (size_t)S.R * p->Mb * p->Nb * sizeof(float));
+        }
+    }
+    p->ws_bytes = off;
+    p->bt_bytes = classical ? 0 : (size_t)S.R * p->Kb * p->Nb * e;
+
+    // ---- info
+    lcma_plan_info& I = p->info;
+    I.algo = p->algo;
+    I.variant = variant;
+    I.m = S.m; I.k = S.k; I.n = S.n; I.R = S.R;
+    I.depth = p->scheme_id == SCHEME_STRASSEN ? 1 : p->scheme_id == SCHEME_STRASSEN2 ? 2 : (classical ? 0 : 1);
+    std::snprintf(I.scheme, sizeof(I.scheme), "%s", S.name.c_str());
+    I.Mb = p->Mb; I.Nb = p->Nb; I.Kb = p->Kb;
+    I.BM = d.dtype == LCMA_FP32 ? 128 : kBM;
+    I.BN = d.dtype == LCMA_FP32 ? 128 : kBN;
+    I.BK = p->BK;
+    I.t_pred_classical = dec.t_std;
+    if (classical) {
+        I.t_pred_choice = dec.t_std;
+    } else {
+        I.t_pred_choice = estimate_time(S, (double)d.M, (double)d.N, (double)d.K, p->hw,
+                                        variant != LCMA_VARIANT_UNFUSED, d.b_static != 0);
+    }
+    I.speedup_pred = I.t_pred_classical / I.t_pred_choice;
+    I.memory_bound = dec.memory_bound;
+    const double ratio = p->hw.flops_mul / p->hw.beta;
+    I.lcma_condition = !classical && condition_lhs(S, (double)d.M, (double)d.N, (double)d.K, false) > ratio;
+    I.fused_condition = !classical && condition_lhs(S, (double)d.M, (double)d.N, (double)d.K, true) > ratio;
+    I.workspace_bytes = p->ws_bytes;
+    I.btilde_bytes = p->bt_bytes;
+    *out = p;
+    return LCMA_OK;
+}
+
+extern "C" lcma_status lcma_plan(int64_t M, int64_t N, int64_t K, lcma_dtype dtype, lcma_algo algo,
+                                 lcma_plan_t* out) {
+    lcma_plan_desc d;
+    std::memset(&d, 0, sizeof(d));
+    d.M = M; d.N = N; d.K = K;
+    d.dtype = dtype;
+    d.out_dtype = (dtype == LCMA_TF32) ? LCMA_FP32 : dtype;
+    d.algo = algo;
+    return lcma_plan_ex(&d, out);
+}
+
+extern "C" void lcma_free(lcma_plan_t p) { delete p; }
+
+extern "C" lcma_status lcma_plan_get_info(lcma_plan_t p, lcma_plan_info* out) {
+    if (!p || !out) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    *out = p->info;
+    return LCMA_OK;
+}
+extern "C" lcma_status lcma_workspace_size(lcma_plan_t p, size_t* bytes) {
+    if (!p || !bytes) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    *bytes = p->ws_bytes;
+    return LCMA_OK;
+}
+extern "C" lcma_status lcma_btilde_size(lcma_plan_t p, size_t* bytes) {
+    if (!p || !bytes) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    *bytes = p->bt_bytes;
+    return LCMA_OK;
+}
+
+extern "C" lcma_status lcma_plan_schedule(lcma_plan_t p, int32_t cta, int32_t* units, int32_t cap,
+                                          int32_t* n) {
+    if (!p || !n) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    if (p->ctas <= 0 || cta < 0 || cta >= p->ctas) return fail(LCMA_ERR_INVALID_VALUE, "bad cta");
+    auto us = host_units(p, cta);
+    *n = (int32_t)us.size();
+    for (int i = 0; i < (int)us.size() && i < cap && units; ++i) {
+        units[4 * i] = us[i].g;
+        units[4 * i + 1] = us[i].r0;
+        units[4 * i + 2] = us[i].r1;
+        units[4 * i + 3] = us[i].role;
+    }
+    return LCMA_OK;
+}
+
+extern "C" lcma_status lcma_decide(int64_t M, int64_t N, int64_t K, lcma_dtype dtype,
+                                   const lcma_hw_profile* hw, int32_t fused, lcma_plan_info* out) {
+    if (!out) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    if (M < 1 || N < 1 || K < 1) return fail(LCMA_ERR_INVALID_VALUE, "M, N, K must be >= 1");
+    Profile P = hw ? Profile{hw->flops_mul, hw->flops_add, hw->beta_elems} : default_profile((int)dtype);
+    if (!(P.flops_mul > 0 && P.flops_add > 0 && P.beta > 0))
+        return fail(LCMA_ERR_INVALID_VALUE, "hardware profile entries must be > 0");
+    std::vector<int> cands = {SCHEME_STRASSEN, SCHEME_STRASSEN2, SCHEME_LADERMAN};
+    DecisionResult dec = decide(cands, (double)M, (double)N, (double)K, P, fused != 0, false);
+    std::memset(out, 0, sizeof(*out));
+    const Scheme* s = scheme_get(dec.scheme_id);
+    out->algo = dec.scheme_id == SCHEME_CLASSICAL ? LCMA_ALGO_CLASSICAL
+                : dec.scheme_id == SCHEME_STRASSEN ? LCMA_ALGO_STRASSEN
+                : dec.scheme_id == SCHEME_STRASSEN2 ? LCMA_ALGO_STRASSEN2
+                                                     : LCMA_ALGO_LADERMAN;
+    out->m = s->m; out->k = s->k; out->n = s->n; out->R = s->R;
+    std::snprintf(out->scheme, sizeof(out->scheme), "%s", s->name.c_str());
+    out->t_pred_classical = dec.t_std;
+    out->t_pred_choice = dec.t_choice;
+    out->speedup_pred = dec.t_std / dec.t_choice;
+    out->memory_bound = dec.memory_bound;
+    const double ratio = P.flops_mul / P.beta;
+    const Scheme* st = scheme_get(SCHEME_STRASSEN);
+    const Scheme* ref = dec.scheme_id == SCHEME_CLASSICAL ? st : s;
+    out->lcma_condition = condition_lhs(*ref, (double)M, (double)N, (double)K, false) > ratio;
+    out->fused_condition = condition_lhs(*ref, (double)M, (double)N, (double)K, true) > ratio;
+    return LCMA_OK;
+}
+
+// ---------------------------------------------------------------- schemes
+extern "C" lcma_status lcma_scheme_register(int32_t m, int32_t k, int32_t n, int32_t R,
+                                            const int8_t* U, const int8_t* V, const int8_t* W,
+                                            const char* name, int32_t* scheme_id) {
+    if (!U || !V || !W || !scheme_id) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    if (m < 1 || k < 1 || n < 1 || R < 1 || m > 16 || k > 16 || n > 16 || R > 4096)
+        return fail(LCMA_ERR_INVALID_VALUE, "bad scheme dimensions");
+    Scheme s;
+    s.name = name ? name : "registered";
+    s.m = m; s.k = k; s.n = n; s.R = R;
+    s.U.assign(U, U + (size_t)R * m * k);
+    s.V.assign(V, V + (size_t)R * k * n);
+    s.W.assign(W, W + (size_t)R * m * n);
+    std::string err;
+    int id = scheme_register(s, err);
+    if (id < 0) return fail((lcma_status)(-id), err);
+    *scheme_id = id;
+    return LCMA_OK;
+}
+
+extern "C" lcma_status lcma_scheme_register_file(const char* path, int32_t* scheme_id) {
+    if (!path || !scheme_id) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    std::ifstream f(path);
+    if (!f) return fail(LCMA_ERR_INVALID_VALUE, std::string("cannot open ") + path);
+    std::stringstream ss;
+    ss << f.rdbuf();
+    Scheme s;
+    std::string err;
+    int rc = scheme_parse(ss.str(), s, err);
+    if (rc < 0) return fail((lcma_status)(-rc), err);
+    s.name = path;
+    int id = scheme_register(s, err);
+    if (id < 0) return fail((lcma_status)(-id), err);
+    *scheme_id = id;
+    return LCMA_OK;
+}
+
+extern "C" lcma_status lcma_scheme_get(int32_t id, int32_t* mknR, int8_t* U, int8_t* V, int8_t* W) {
+    const Scheme* s = scheme_get(id);
+    if (!s) return fail(LCMA_ERR_INVALID_VALUE, "unknown scheme id");
+    if (mknR) { mknR[0] = s->m; mknR[1] = s->k; mknR[2] = s->n; mknR[3] = s->R; }
+    if (U) std::memcpy(U, s->U.data(), s->U.size());
+    if (V) std::memcpy(V, s->V.data(), s->V.size());
+    if (W) std::memcpy(W, s->W.data(), s->W.size());
+    return LCMA_OK;
+}
+
+extern "C" const char* lcma_last_error(void) { return t_err.c_str(); }
+extern "C" int32_t lcma_last_launch_count(void) { return t_launches; }
+
+// ---------------------------------------------------------------- launching
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+lcma_status make_map(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64_t cols, uint64_t rows,
+                     uint32_t box_c, uint32_t box_r) {
+    auto fn = encode_fn();
+    if (!fn) return fail(LCMA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMapDataType t = dt == LCMA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                            : dt == LCMA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const int e = elem_bytes(dt);
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * (cuuint64_t)e};
+    cuuint32_t box[2] = {box_c, box_r};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, t, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[160];
+        std::snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d) dims %llu x %llu box %u x %u",
+                      (int)r, (unsigned long long)cols, (unsigned long long)rows, box_c, box_r);
+        return fail(LCMA_ERR_CUDA, buf);
+    }
+    return LCMA_OK;
+}
+
+lcma_status check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    ++t_launches;
+    return LCMA_OK;
+}
+
+lcma_status ensure_smem_attr() {
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [] {
+        err = cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemBytes);
+    });
+    if (err != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
+    return LCMA_OK;
+}
+
+int grid_for(long long work, int per_block) {
+    long long b = (work + per_block - 1) / per_block;
+    if (b < 1) b = 1;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)b;
+}
+
+// Group combine of one operand into dst[R][E0][E1] (Alg. 2 stage 1 or 2).
+lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, bool is_b,
+                           cudaStream_t st) {
+    const Scheme& S = p->sch;
+    CombineParams c;
+    std::memset(&c, 0, sizeof(c));
+    c.src = src;
+    c.dst = dst;
+    c.R = S.R;
+    c.elem = p->d.dtype == LCMA_BF16 ? ELEM_BF16 : p->d.dtype == LCMA_FP16 ? ELEM_FP16 : ELEM_FP32;
+    c.round_tf32 = p->d.dtype == LCMA_TF32;
+    int P, Q;
+    if (!is_b) {                      // A (M x K): blocks (i, l), coef U[r][i][l]
+        c.rows = p->d.M; c.cols = p->d.K; c.E0 = p->Mb; c.E1 = p->Kb; P = S.m; Q = S.k;
+    } else if (p->d.b_layout == 0) {  // B (K x N): blocks (l, j), coef V[r][l][j]
+        c.rows = p->d.K; c.cols = p->d.N; c.E0 = p->Kb; c.E1 = p->Nb; P = S.k; Q = S.n;
+    } else {                          // B (N x K): blocks (j, l), coef V[r][l][j]
+        c.rows = p->d.N; c.cols = p->d.K; c.E0 = p->Nb; c.E1 = p->Kb; P = S.n; Q = S.k;
+    }
+    c.P = P;
+    c.Q = Q;
+    const int pq = P * Q;
+    const int inst = pq <= 4 ? 4 : pq <= 9 ? 9 : pq <= 16 ? 16 : pq <= 25 ? 25 : 32;
+    if (S.R > kCombMaxR || pq > kCombMaxPQ) return fail(LCMA_ERR_NOT_SUPPORTED, "scheme too large");
+    for (int r = 0; r < S.R; ++r)
+        for (int a = 0; a < P; ++a)
+            for (int b = 0; b < Q; ++b) {
+                int8_t v;
+                if (!is_b) v = S.u(r, a, b);
+                else if (p->d.b_layout == 0) v = S.v(r, a, b);
+                else v = S.v(r, b, a);
+                c.coef[r * inst + a * Q + b] = v;
+            }
+    const bool fp32 = c.elem == ELEM_FP32;
+    const int vec = (fp32 || inst > 9) ? 4 : 8;
+    const long long nvec = c.E0 * (c.E1 / vec);
+    const int grid = grid_for(nvec, 256);
+#define LCMA_COMB(V, PQ) group_combine_kernel<V, PQ><<<grid, 256, 0, st>>>(c)
+    if (vec == 8) {
+        if (inst == 4) LCMA_COMB(8, 4); else LCMA_COMB(8, 9);
+    } else {
+        if (inst == 4) LCMA_COMB(4, 4);
+        else if (inst == 9) LCMA_COMB(4, 9);
+        else if (inst == 16) LCMA_COMB(4, 16);
+        else if (inst == 25) LCMA_COMB(4, 25);
+        else LCMA_COMB(4, 32);
+    }
+#undef LCMA_COMB
+    return check_launch("group_combine_kernel");
+}
+
+lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cudaStream_t st) {
+    const Scheme& S = p->sch;
+    CombineHParams c;
+    std::memset(&c, 0, sizeof(c));
+    c.H = H; c.C = C;
+    c.M = p->d.M; c.N = p->d.N; c.Mb = p->Mb; c.Nb = p->Nb; c.ldc = p->d.N;
+    c.m = S.m; c.n = S.n; c.R = S.R;
+    c.out_type = p->d.out_dtype == LCMA_FP32 || p->d.out_dtype == LCMA_TF32 ? 2
+                 : p->d.out_dtype == LCMA_BF16 ? 0 : 1;
+    const int mn = S.m * S.n;
+    const int inst = mn <= 1 ? 1 : mn <= 4 ? 4 : mn <= 9 ? 9 : mn <= 16 ? 16 : mn <= 25 ? 25 : 32;
+    for (int r = 0; r < S.R; ++r)
+        for (int ij = 0; ij < mn; ++ij) c.Wc[r * inst + ij] = S.W[(size_t)r * mn + ij];
+    const long long nvec = c.Mb * (c.Nb / 4);
+    const int grid = grid_for(nvec, 256);
+    switch (inst) {
+        case 1: group_combine_h_kernel<1><<<grid, 256, 0, st>>>(c); break;
+        case 4: group_combine_h_kernel<4><<<grid, 256, 0, st>>>(c); break;
+        case 9: group_combine_h_kernel<9><<<grid, 256, 0, st>>>(c); break;
+        case 16: group_combine_h_kernel<16><<<grid, 256, 0, st>>>(c); break;
+        case 25: group_combine_h_kernel<25><<<grid, 256, 0, st>>>(c); break;
+        default: group_combine_h_kernel<32><<<grid, 256, 0, st>>>(c); break;
+    }
+    return check_launch("group_combine_h_kernel");
+}
+
+// tcgen05 GEMM: classical (R == 1 over A, B) or the LCMA GEMM stage over the
+// materialised At / Bt with the fused Combine H (or H store) epilogue.
+lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, void* C, float* P,
+                        int* flags, float* H, cudaStream_t st) {
+    lcma_status rs = ensure_smem_attr();
+    if (rs != LCMA_OK) return rs;
+    const Scheme& S = p->sch;
+    const bool classical = p->scheme_id == SCHEME_CLASSICAL;
+    const lcma_dtype dt = p->d.dtype;
+    const int epr = 128 / p->e;           // elements per 128-byte row
+    CUtensorMap ta, tb;
+    // A operand: K-major rows
+    const uint64_t a_cols = classical ? p->d.K : p->Kb;
+    const uint64_t a_rows = classical ? p->d.M : (uint64_t)S.R * p->Mb;
+    rs = make_map(&ta, Aop, dt, a_cols, a_rows, epr, kBM);
+    if (rs != LCMA_OK) return rs;
+    const bool b_mn = p->d.b_layout == 0;
+    if (!b_mn) {   // N x K (K-major)
+        const uint64_t cols = classical ? p->d.K : p->Kb;
+        const uint64_t rows = classical ? p->d.N : (uint64_t)S.R * p->Nb;
+        rs = make_map(&tb, Bop, dt, cols, rows, epr, kBN);
+    } else {       // K x N (MN-major): boxes of 128 bytes of N x BK rows
+        const uint64_t cols = classical ? p->d.N : p->Nb;
+        const uint64_t rows = classical ? p->d.K : (uint64_t)S.R * p->Kb;
+        rs = make_map(&tb, Bop, dt, cols, rows, epr, p->BK);
+    }
+    if (rs != LCMA_OK) return rs;
+
+    GemmParams g;
+    std::memset(&g, 0, sizeof(g));
+    g.nX = p->nX; g.nZ = p->nZ; g.G = p->G; g.R = S.R; g.nK = p->nK; g.BK = p->BK;
+    g.a_rows_per_r = classical ? 0 : (int)p->Mb;
+    g.b_rows_per_r = classical ? 0 : (int)(b_mn ? p->Kb : p->Nb);
+    g.b_mn_major = b_mn;
+    g.tf32 = dt == LCMA_TF32;
+    g.idesc = ptx::make_idesc(dt == LCMA_BF16 ? 1u : dt == LCMA_FP16 ? 0u : 2u, kBM, kBN, b_mn ? 1u : 0u, 0u);
+    g.W = p->ctas; g.q = p->q; g.tail_c = p->tail_c; g.swz = p->swz;
+    g.epi_mode = H ? EPI_STORE_H : EPI_FUSED;
+    g.out_type = (p->d.out_dtype == LCMA_FP32 || p->d.out_dtype == LCMA_TF32) ? OUT_FP32
+                 : p->d.out_dtype == LCMA_BF16 ? OUT_BF16 : OUT_FP16;
+    g.m = S.m; g.n = S.n;
+    g.M = p->d.M; g.N = p->d.N; g.Mb = p->Mb; g.Nb = p->Nb; g.ldc = p->d.N;
+    g.C = C; g.P = P; g.flags = flags; g.H = H;
+    const int mn = S.m * S.n;
+    if (S.R > kMaxR || mn > kMaxMN) return fail(LCMA_ERR_NOT_SUPPORTED, "scheme too large for the fused kernel");
+    for (int r = 0; r < S.R; ++r)
+        for (int ij = 0; ij < mn; ++ij) g.Wc[r * mn + ij] = S.W[(size_t)r * mn + ij];
+    umma_gemm_kernel<<<p->ctas, kThreads, kSmemBytes, st>>>(ta, tb, g);
+    return check_launch("umma_gemm_kernel");
+}
+
+lcma_status launch_simt(const lcma_plan_s* p, const float* A, const float* B, float* H,
+                        cudaStream_t st) {
+    const Scheme& S = p->sch;
+    const bool classical = p->scheme_id == SCHEME_CLASSICAL;
+    SimtParams s;
+    std::memset(&s, 0, sizeof(s));
+    s.A = A; s.B = B; s.H = H;
+    s.b_kmajor = p->d.b_layout == 1;
+    if (classical) {
+        s.Mr = p->d.M; s.Nr = p->d.N; s.Kr = p->d.K;
+        s.lda = p->d.K; s.ldb = s.b_kmajor ? p->d.K : p->d.N; s.ldh = p->d.N;
+    } else {
+        s.Mr = p->Mb; s.Nr = p->Nb; s.Kr = p->Kb;
+        s.lda = p->Kb; s.ldb = s.b_kmajor ? p->Kb : p->Nb; s.ldh = p->Nb;
+        s.sAr = p->Mb * p->Kb; s.sBr = p->Kb * p->Nb; s.sHr = p->Mb * p->Nb;
+    }
+    dim3 grid((unsigned)cdiv(s.Nr, 128), (unsigned)cdiv(s.Mr, 128), classical ? 1 : S.R);
+    simt_sgemm_batched_kernel<<<grid, 256, 0, st>>>(s);
+    return check_launch("simt_sgemm_batched_kernel");
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+    auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return na && nb && x < y + nb && y < x + na;
+}
+
+lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user, void* C, void* ws,
+                size_t ws_bytes, void* stream) {
+    t_err.clear();
+    t_launches = 0;
+    if (!p || !A || !C || (!B && !Bt_user)) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    auto mis = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) != 0; };
+    if (mis(A) || mis(C) || (B && mis(B)) || (Bt_user && mis(Bt_user)) || (ws && mis(ws)))
+        return fail(LCMA_ERR_MISALIGNED, "device pointers must be 16-byte aligned");
+    if (ws_bytes < p->ws_bytes || (p->ws_bytes && !ws))
+        return fail(LCMA_ERR_WORKSPACE, "workspace smaller than lcma_workspace_size()");
+    const size_t eo = (p->d.out_dtype == LCMA_FP32 || p->d.out_dtype == LCMA_TF32) ? 4 : p->e;
+    const size_t cb = (size_t)p->d.M * p->d.N * eo;
+    if (overlaps(C, cb, A, (size_t)p->d.M * p->d.K * p->e) ||
+        (B && overlaps(C, cb, B, (size_t)p->d.K * p->d.N * p->e)) ||
+        overlaps(C, cb, ws, p->ws_bytes))
+        return fail(LCMA_ERR_INVALID_VALUE, "C must not overlap A, B or the workspace");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    uint8_t* w = reinterpret_cast<uint8_t*>(ws);
+    const bool classical = p->scheme_id == SCHEME_CLASSICAL;
+    const bool fp32 = p->d.dtype == LCMA_FP32;
+    if (classical) {
+        if (fp32) {
+            if (p->d.out_dtype != LCMA_FP32) return fail(LCMA_ERR_NOT_SUPPORTED, "fp32 output only");
+            return launch_simt(p, (const float*)A, (const float*)B, (float*)C, st);
+        }
+        return launch_umma(p, A, B, C, nullptr, nullptr, nullptr, st);
+    }
+    void* At = w + p->off_At;
+    const void* Bt = Bt_user;
+    lcma_status rs = launch_combine(p, A, At, false, st);          // Combine A (Eq. 3)
+    if (rs != LCMA_OK) return rs;
+    if (!Bt) {
+        rs = launch_combine(p, B, w + p->off_Bt, true, st);        // Combine B (Eq. 4)
+        if (rs != LCMA_OK) return rs;
+        Bt = w + p->off_Bt;
+    }
+    if (fp32) {
+        float* H = reinterpret_cast<float*>(w + p->off_H);
+        rs = launch_simt(p, (const float*)At, (const float*)Bt, H, st);   // Eq. 5
+        if (rs != LCMA_OK) return rs;
+        return launch_combine_h(p, H, C, st);                              // Eq. 6
+    }
+    if (p->variant == LCMA_VARIANT_UNFUSED) {
+        float* H = reinterpret_cast<float*>(w + p->off_H);
+        rs = launch_umma(p, At, Bt, C, nullptr, nullptr, H, st);
+        if (rs != LCMA_OK) return rs;
+        return launch_combine_h(p, H, C, st);
+    }
+    return launch_umma(p, At, Bt, C, reinterpret_cast<float*>(w + p->off_P),
+                       reinterpret_cast<int*>(w + p->off_flags), nullptr, st);
+}
+
+}  // namespace
+
+extern "C" lcma_status lcma_gemm(lcma_plan_t p, const void* A, const void* B, void* C, void* ws,
+                                 size_t ws_bytes, void* stream) {
+    if (p && !B) return fail(LCMA_ERR_INVALID_VALUE, "null B");
+    return run(p, A, B, nullptr, C, ws, ws_bytes, stream);
+}
+
+extern "C" lcma_status lcma_gemm_precombined(lcma_plan_t p, const void* A, const void* Bt, void* C,
+                                             void* ws, size_t ws_bytes, void* stream) {
+    if (!p || !Bt) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    if (p->scheme_id == SCHEME_CLASSICAL) return run(p, A, Bt, nullptr, C, ws, ws_bytes, stream);
+    return run(p, A, nullptr, Bt, C, ws, ws_bytes, stream);
+}
+
+extern "C" lcma_status lcma_precombine_b(lcma_plan_t p, const void* B, void* Bt, void* stream) {
+    t_err.clear();
+    t_launches = 0;
+    if (!p || !B || !Bt) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
+    if ((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(Bt)) & 15)
+        return fail(LCMA_ERR_MISALIGNED, "device pointers must be 16-byte aligned");
+    if (p->scheme_id == SCHEME_CLASSICAL) return fail(LCMA_ERR_INVALID_VALUE, "classical plan has no Bt");
+    return launch_combine(p, B, Bt, true, reinterpret_cast<cudaStream_t>(stream));
+}

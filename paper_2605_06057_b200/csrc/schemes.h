@@ -1,0 +1,39 @@
+// schemes.h -- LCMA scheme registry of the product library (host).
+// An LCMA is the tuple <m,k,n,R,U,V,W>; U[r][i][l] multiplies
+// A_{i,l} (Eq. 3), V[r][l][j] multiplies B_{l,j} (Eq. 4), W[r][i][j] adds H_r
+// into C_{i,j} (Eq. 6).  Coefficients restricted to {-1,0,1}.
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace lcma {
+
+struct Scheme {
+    std::string name;
+    int m = 1, k = 1, n = 1, R = 1;
+    std::vector<int8_t> U, V, W;   // R*m*k, R*k*n, R*m*n
+    int8_t u(int r, int i, int l) const { return U[(r * m + i) * k + l]; }
+    int8_t v(int r, int l, int j) const { return V[(r * k + l) * n + j]; }
+    int8_t w(int r, int i, int j) const { return W[(r * m + i) * n + j]; }
+    int nnzU() const;
+    int nnzV() const;
+    int nnzW() const;
+};
+
+// Built-in ids: 0 classical <1,1,1;1>, 1 Strassen, 2 Strassen^2, 3 Laderman.
+enum : int { SCHEME_CLASSICAL = 0, SCHEME_STRASSEN = 1, SCHEME_STRASSEN2 = 2, SCHEME_LADERMAN = 3 };
+
+// Returns nullptr for an unknown id.  Thread-safe.
+const Scheme* scheme_get(int id);
+// Validates (Brent identity, coefficient range, size limits) and registers.
+// On failure returns a negative lcma_status and fills `err`.
+int scheme_register(const Scheme& s, std::string& err);
+// Text format of SPEC S:143-145.
+int scheme_parse(const std::string& text, Scheme& out, std::string& err);
+// Exact Brent check; returns number of failing tuples, first failure in `err`.
+long long scheme_brent_failures(const Scheme& s, std::string* first);
+Scheme scheme_compose(const Scheme& outer, const Scheme& inner);
+
+}  // namespace lcma
