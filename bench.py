@@ -1,0 +1,363 @@
+#!/usr/bin/env python3
+"""bench.py -- effective TFLOP/s (2MNK/t) of the LCMA hot path on B200.
+
+One *step* = one pass of the whole hot path over one batch of synthetic input:
+host-side plan/decision is done once outside the timed region (P:161-263,
+"once per shape"); each step runs Combine A, Combine B, the R-way tcgen05
+sub-GEMM with the fused Combine H epilogue (Alg. 2) through the
+library's C ABI (lcma_gemm).  Default workload: BASELINE.json configs[1] (cfg2,
+Llama-3-8B FFN up-proj M=8192 N=14336 K=4096 bf16, Strassen <2,2,2;7>).
+
+Multi-GPU (torchrun, one process per GPU): block-row partition of A and C
+(SURVEY 8(e)); every rank computes its own 8192-row block with no data-path
+collective -> weak scaling.
+
+`--impl reference` times the CPU oracle (naive fp64 GEMM, oracle/) on a
+bounded row sample on the host cores -- the reference arm of this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG2 = dict(M=8192, N=14336, K=4096)
+BASELINE_DESC = ("cfg2: Llama-3-8B FFN up-proj GEMM M=8192 N=14336 K=4096 bf16 "
+                 "(BASELINE.json configs[1])")
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, \
+        "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_oracle_sample(M, N, K, seconds=15.0, seed_a=201, seed_b=202):
+    """Time the oracle's naive fp64 GEMM (oracle.gemm_rows_f64) on a bounded
+    row sample of the workload; returns (TFLOP/s, rows, threads, seconds)."""
+    import numpy as np
+    import oracle as O
+    from paper_2605_06057_b200 import inputs
+    rng = np.random.default_rng(0)
+    B = inputs.matrix(K, N, 0, seed_b).double().numpy()
+    rows = 8
+    A = inputs.matrix(M, K, 0, seed_a).double().numpy()
+    O.gemm_rows_f64(A, B, [0])                      # load / warm
+    while True:
+        idx = np.sort(rng.choice(M, rows, replace=False))
+        t0 = time.perf_counter()
+        O.gemm_rows_f64(A, B, idx)
+        dt = time.perf_counter() - t0
+        if dt * 4 >= seconds or rows >= M:
+            break
+        rows = min(M, rows * max(2, int(seconds / max(dt, 1e-3) / 4)))
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return 2.0 * rows * N * K / dt / 1e12, rows, threads, dt
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle on the host cores, same metric/unit."""
+    world, rank, _ = _dist_init()
+    if rank != 0:
+        return 0
+    M, N, K = CFG2["M"], CFG2["N"], CFG2["K"]
+    import numpy as np
+    import oracle as O
+    from paper_2605_06057_b200 import inputs
+    A = inputs.matrix(M, K, 0, 201).double().numpy()
+    B = inputs.matrix(K, N, 0, 202).double().numpy()
+    rows = int(args.ref_rows)
+    rng = np.random.default_rng(1)
+    times = []
+    for it in range(args.warmup + args.steps):
+        idx = np.sort(rng.choice(M, rows, replace=False))
+        t0 = time.perf_counter()
+        O.gemm_rows_f64(A, B, idx)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    value = 2.0 * rows * N * K / t / 1e12
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    sample = f"{rows} random rows of the cfg2 GEMM per step (naive fp64 i-k-j oracle, OpenMP)"
+    line = {
+        "impl": "reference", "metric": "effective TFLOP/s (2MNK/t)", "value": value,
+        "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": BASELINE_DESC + " -- CPU oracle row sample", "rows_per_step": rows},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2605_06057_b200 as L
+    from paper_2605_06057_b200 import inputs
+
+    world, rank, local = _dist_init()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+
+    M, N, K = CFG2["M"], CFG2["N"], CFG2["K"]
+    algo = args.algo
+    # rank's block-row shard of the global (M*world) x N problem; B replicated
+    A_h, B_h = inputs.operands(M, N, K, L.BF16, 510 + rank, 502, b_layout=args.b_layout)
+    A = A_h.cuda()
+    B = B_h.cuda()
+    plan = L.Plan(M, N, K, dtype=L.BF16, algo=algo, b_layout=args.b_layout, variant=args.variant,
+                  b_static=args.static_b)
+    ws = plan.workspace()
+    C = plan.empty_c()
+    Bt = plan.precombine_b(B) if (args.static_b and plan.info["algo"] != L.ALGO["classical"]) else None
+
+    def step():
+        if Bt is not None:
+            plan.gemm_precombined(A, Bt, C, ws)
+        else:
+            plan.gemm(A, B, C, ws)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(max(3, args.warmup)):
+        step()
+    launches_per_step = L.Plan.last_launch_count()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, inputs (400 MB) larger than L2 (126 MB)
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        L.set_kernel_events(*k_ev[i])
+        step()
+    L.set_kernel_events(None, None)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    ms = t0.elapsed_time(t1) / args.steps
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in k_ev)
+    if world > 1:
+        tt = torch.tensor([ms, k_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, k_ms = float(tt[0]), float(tt[1])
+    flops = 2.0 * M * N * K
+    value = world * flops / (ms * 1e-3) / 1e12
+
+    # ---- classical tcgen05 kernel on the same box (the no-LCMA reference)
+    ref = {}
+    if rank == 0 and not args.no_classical and plan.info["algo"] != L.ALGO["classical"]:
+        cp = L.Plan(M, N, K, dtype=L.BF16, algo="classical", b_layout=args.b_layout)
+        Cc = cp.empty_c()
+        for _ in range(3):
+            cp.gemm(A, B, Cc)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            cp.gemm(A, B, Cc)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        cms = e0.elapsed_time(e1) / args.steps
+        ref = {"classical_tcgen05_tflops": flops / (cms * 1e-3) / 1e12, "classical_ms": cms}
+        del Cc
+
+    # ---- end to end through the public API with HOST buffers
+    e2e = None
+    if not args.no_e2e:
+        A_pin = A_h.pin_memory()
+        B_pin = B_h.pin_memory()
+        C_pin = torch.empty(C.shape, dtype=C.dtype, pin_memory=True)
+        Ad = torch.empty_like(A)
+        Bd = torch.empty_like(B)
+        for _ in range(2):
+            Ad.copy_(A_pin, non_blocking=True)
+            Bd.copy_(B_pin, non_blocking=True)
+            plan.gemm(Ad, Bd, C, ws)
+            C_pin.copy_(C, non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(1, min(args.steps, 10))
+        e0.record(stream)
+        for _ in range(n_e2e):
+            Ad.copy_(A_pin, non_blocking=True)
+            Bd.copy_(B_pin, non_blocking=True)
+            plan.gemm(Ad, Bd, C, ws)
+            C_pin.copy_(C, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / n_e2e
+        if world > 1:
+            tt = torch.tensor([ems], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt[0])
+        e2e = {"value": world * flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": A_h.numel() * 2 + B_h.numel() * 2,
+               "d2h_bytes_per_step": C.numel() * C.element_size(), "ms_per_step": ems}
+
+    if rank == 0:
+        peaks, peak_src = _peaks()
+        info = plan.info
+        R = info["R"]
+        real_flops = 2.0 * R * info["Mb"] * info["Nb"] * info["Kb"] if info["algo"] != L.ALGO["classical"] \
+            else flops
+        achieved = real_flops / (k_ms * 1e-3) / 1e12
+        peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                tj = json.load(f)
+            key = f"{info['scheme']}|{args.variant}|static{int(bool(args.static_b))}|bl{args.b_layout}"
+            traffic = tj.get(key)
+        cpu = None
+        if not args.no_cpu and world == 1:
+            v, rows, threads, dt = cpu_oracle_sample(M, N, K, seconds=args.cpu_seconds)
+            cpu = {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                   "sample": f"{rows} random rows of the cfg2 GEMM, naive fp64 i-k-j oracle "
+                             f"(oracle.gemm_rows_f64, OpenMP), {dt:.1f} s"}
+        line = {
+            "metric": "effective TFLOP/s (2MNK/t)",
+            "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": BASELINE_DESC, "algo": info["scheme"],
+                       "variant": {1: "unfused", 2: "fused_h", 3: "producer", 0: "classical"}[info["variant"]],
+                       "static_b": bool(args.static_b), "b_layout": "KxN" if args.b_layout == 0 else "NxK",
+                       "M_per_rank": M, "N": N, "K": K, "parallelism": f"block-rows x{world}",
+                       "cta_group": info["cta_group"], "waves": info["waves"],
+                       "l2": "inputs+output 400 MB > 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "tensor", "kernel": "umma_gemm_kernel", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": traffic,
+                         "note": f"achieved = real MMA flops 2R*Mb*Nb*Kb per launch / live CUDA-event "
+                                 f"kernel time ({k_ms:.3f} ms); peak = bf16 sustained, {peak_src}"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "effective_vs_classical": (value / world) / ref["classical_tcgen05_tflops"] if ref else None,
+        }
+        line.update(ref)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--algo", default="strassen")
+    ap.add_argument("--variant", default="auto")
+    ap.add_argument("--static_b", type=int, default=0)
+    ap.add_argument("--b_layout", type=int, default=0)
+    ap.add_argument("--no_classical", action="store_true")
+    ap.add_argument("--no_e2e", action="store_true")
+    ap.add_argument("--no_cpu", action="store_true")
+    ap.add_argument("--cpu_seconds", type=float, default=15.0)
+    ap.add_argument("--ref_rows", type=int, default=64)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -109,6 +109,7 @@ typedef struct {
     char scheme[64];
     int64_t Mb, Nb, Kb;       /* padded block extents (>= ceil(M/m) etc.)  */
     int32_t BM, BN, BK;
+    int32_t cta_group;        /* 1: cta_group::1 128-row tiles, 2: CTA pairs, 256-row tiles */
     int32_t groups, tiles, ctas, waves, group_waves, split_groups;
     double t_pred_classical, t_pred_choice, speedup_pred;  /* seconds, model      */
     int32_t memory_bound;     /* Eq. stdgemm held                          */
@@ -160,6 +161,15 @@ lcma_status lcma_scheme_get(int32_t scheme_id, int32_t* mknR, int8_t* U, int8_t*
  * segment) and returns the count in *n. */
 lcma_status lcma_plan_schedule(lcma_plan_t plan, int32_t cta, int32_t* units, int32_t cap,
                                int32_t* n);
+
+/* Measurement hook: when non-NULL cudaEvent_t handles are set, each later
+ * lcma_gemm* call on this thread records ev_start / ev_end on its stream right
+ * before / after the tcgen05 GEMM kernel (the dominant kernel), so callers
+ * can time it live with CUDA events.  NULL, NULL disables. */
+void lcma_set_kernel_events(void* ev_start, void* ev_end);
+/* Diagnostics (LCMA_STATS=1 in the environment): copies n per-CTA wait-cycle
+ * counters to host memory; returns 0 on success. */
+int lcma_debug_stats(unsigned long long* host, int n);
 
 /* Thread-local message for the last error on this thread ("" if none). */
 const char* lcma_last_error(void);

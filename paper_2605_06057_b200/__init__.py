@@ -50,7 +50,7 @@ class PlanInfo(ctypes.Structure):
                 ("R", ctypes.c_int32), ("depth", ctypes.c_int32), ("scheme", ctypes.c_char * 64),
                 ("Mb", ctypes.c_int64), ("Nb", ctypes.c_int64), ("Kb", ctypes.c_int64),
                 ("BM", ctypes.c_int32), ("BN", ctypes.c_int32), ("BK", ctypes.c_int32),
-                ("groups", ctypes.c_int32), ("tiles", ctypes.c_int32), ("ctas", ctypes.c_int32),
+                ("cta_group", ctypes.c_int32), ("groups", ctypes.c_int32), ("tiles", ctypes.c_int32), ("ctas", ctypes.c_int32),
                 ("waves", ctypes.c_int32), ("group_waves", ctypes.c_int32),
                 ("split_groups", ctypes.c_int32),
                 ("t_pred_classical", ctypes.c_double), ("t_pred_choice", ctypes.c_double),
@@ -99,6 +99,10 @@ def lib():
     L.lcma_last_error.argtypes = []
     L.lcma_last_launch_count.restype = I32
     L.lcma_last_launch_count.argtypes = []
+    L.lcma_set_kernel_events.argtypes = [P, P]
+    L.lcma_set_kernel_events.restype = None
+    L.lcma_debug_stats.argtypes = [P, ctypes.c_int]
+    L.lcma_debug_stats.restype = ctypes.c_int
     for name in ("lcma_plan", "lcma_plan_ex", "lcma_plan_get_info", "lcma_workspace_size",
                  "lcma_btilde_size", "lcma_gemm", "lcma_precombine_b", "lcma_gemm_precombined",
                  "lcma_decide", "lcma_scheme_register_file", "lcma_scheme_register",
@@ -212,6 +216,12 @@ class Plan:
     @staticmethod
     def last_launch_count():
         return int(lib().lcma_last_launch_count())
+
+
+def set_kernel_events(start=None, end=None):
+    """Record torch.cuda.Event `start`/`end` around the tcgen05 GEMM of later calls."""
+    lib().lcma_set_kernel_events(start.cuda_event if start is not None else None,
+                                 end.cuda_event if end is not None else None)
 
 
 def decide(M, N, K, dtype=BF16, hw=None, fused=True):

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <mutex>
@@ -24,6 +25,8 @@ namespace {
 
 thread_local std::string t_err;
 thread_local int t_launches = 0;
+// optional CUDA events recorded around the tcgen05 GEMM launch (lcma_set_kernel_events)
+thread_local cudaEvent_t t_ev_start = nullptr, t_ev_end = nullptr;
 
 lcma_status fail(lcma_status st, const std::string& msg) {
     t_err = msg;
@@ -46,6 +49,35 @@ int device_sm_count() {
     return sms;
 }
 
+// Co-resident clusters of 2 for umma_gemm_kernel<2> (0 if unknown / no GPU).
+int max_active_pairs() {
+    static int cached = -1;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cached = 0;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
+        if (cudaFuncSetAttribute(umma_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg<2>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return; }
+        cudaLaunchConfig_t cfg;
+        std::memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3(2);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = Cfg<2>::kSmemBytes;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, umma_gemm_kernel<2>, &cfg) == cudaSuccess) cached = n;
+        else cudaGetLastError();
+    });
+    return cached;
+}
+
 }  // namespace
 
 struct lcma_plan_s {
@@ -58,7 +90,7 @@ struct lcma_plan_s {
     int64_t Mb, Nb, Kb;
     int BK, e;
     int nX, nZ, G, nK;
-    int ctas, q, tail_c, swz;
+    int ctas, cg, q, tail_c, swz;
     size_t off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
     lcma_plan_info info;
 };
@@ -72,8 +104,9 @@ struct HostUnit { int g, r0, r1, role; };
 std::vector<HostUnit> host_units(const lcma_plan_s* p, int w) {
     std::vector<HostUnit> out;
     const int R = p->sch.R;
-    for (int i = 0; i < p->q; ++i) out.push_back({i * p->ctas + w, 0, R, ROLE_WHOLE});
-    const long long Tt = (long long)(p->G - p->q * p->ctas) * R;
+    const int W = p->ctas / p->cg;
+    for (int i = 0; i < p->q; ++i) out.push_back({i * W + w, 0, R, ROLE_WHOLE});
+    const long long Tt = (long long)(p->G - p->q * W) * R;
     long long t = std::min<long long>((long long)w * p->tail_c, Tt);
     long long t_end = std::min<long long>(t + p->tail_c, Tt);
     while (t < t_end) {
@@ -82,7 +115,7 @@ std::vector<HostUnit> host_units(const lcma_plan_s* p, int w) {
         long long stop = std::min<long long>((gl + 1) * R, t_end);
         int r1 = (int)(stop - gl * R);
         int role = (r0 == 0 && r1 == R) ? ROLE_WHOLE : (r0 == 0 ? ROLE_OWNER : ROLE_CONTRIB);
-        out.push_back({p->q * p->ctas + (int)gl, r0, r1, role});
+        out.push_back({p->q * W + (int)gl, r0, r1, role});
         t = stop;
     }
     return out;
@@ -90,7 +123,7 @@ std::vector<HostUnit> host_units(const lcma_plan_s* p, int w) {
 
 void make_schedule(lcma_plan_s* p, int mode) {
     const int R = p->sch.R;
-    const int W = p->ctas;
+    const int W = p->ctas / p->cg;
     if (mode == 2) {
         p->q = 0;                              // paper: contiguous split-group chunks
     } else {
@@ -101,7 +134,7 @@ void make_schedule(lcma_plan_s* p, int mode) {
     p->swz = 16;
     p->info.groups = p->G;
     p->info.tiles = (int)std::min<long long>((long long)p->G * R, INT32_MAX);
-    p->info.ctas = W;
+    p->info.ctas = p->ctas;
     p->info.waves = p->q * R + (Tt > 0 ? p->tail_c : 0);
     p->info.group_waves = (int)cdiv(p->G, W) * R;
     int splits = 0;
@@ -197,20 +230,34 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         p->nX = p->nZ = p->nK = 0;
         p->G = 0;
         p->ctas = 0;
+        p->cg = 1;
     } else {
         p->BK = 128 / e;
+        const int sms = device_sm_count();
+        p->ctas = d.num_ctas > 0 ? std::min(d.num_ctas, sms) : sms;
+        p->cg = 2;
+        if (const char* e_cg = std::getenv("LCMA_CG")) p->cg = std::atoi(e_cg) == 1 ? 1 : 2;
+        if (p->ctas < 2) p->cg = 1;
+        p->ctas -= p->ctas % p->cg;
+        if (p->cg == 2) {
+            // a persistent grid must be fully co-resident (split groups wait on
+            // each other): use the number of CTA pairs the device can host
+            const int pairs = max_active_pairs();
+            if (pairs > 0) p->ctas = std::min(p->ctas, 2 * pairs);
+        }
+        const int tileM = kBM * p->cg;
         if (classical) {
-            p->nX = (int)cdiv(d.M, kBM);
+            p->nX = (int)cdiv(d.M, tileM);
             p->nZ = (int)cdiv(d.N, kBN);
             p->nK = (int)cdiv(d.K, p->BK);
-            p->Mb = (int64_t)p->nX * kBM;
+            p->Mb = (int64_t)p->nX * tileM;
             p->Nb = (int64_t)p->nZ * kBN;
             p->Kb = (int64_t)p->nK * p->BK;
         } else {
-            p->Mb = roundup(cdiv(d.M, S.m), kBM);
+            p->Mb = roundup(cdiv(d.M, S.m), tileM);
             p->Nb = roundup(cdiv(d.N, S.n), kBN);
             p->Kb = roundup(cdiv(d.K, S.k), p->BK);
-            p->nX = (int)(p->Mb / kBM);
+            p->nX = (int)(p->Mb / tileM);
             p->nZ = (int)(p->Nb / kBN);
             p->nK = (int)(p->Kb / p->BK);
         }
@@ -220,8 +267,6 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             return fail(LCMA_ERR_NOT_SUPPORTED, "problem too large for 32-bit tile coordinates");
         }
         p->G = p->nX * p->nZ;
-        const int sms = device_sm_count();
-        p->ctas = d.num_ctas > 0 ? std::min(d.num_ctas, sms) : sms;
         make_schedule(p, d.schedule == 2 ? 2 : 1);
     }
 
@@ -256,9 +301,10 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     I.depth = p->scheme_id == SCHEME_STRASSEN ? 1 : p->scheme_id == SCHEME_STRASSEN2 ? 2 : (classical ? 0 : 1);
     std::snprintf(I.scheme, sizeof(I.scheme), "%s", S.name.c_str());
     I.Mb = p->Mb; I.Nb = p->Nb; I.Kb = p->Kb;
-    I.BM = d.dtype == LCMA_FP32 ? 128 : kBM;
+    I.BM = d.dtype == LCMA_FP32 ? 128 : kBM * p->cg;
     I.BN = d.dtype == LCMA_FP32 ? 128 : kBN;
     I.BK = p->BK;
+    I.cta_group = p->cg;
     I.t_pred_classical = dec.t_std;
     if (classical) {
         I.t_pred_choice = dec.t_std;
@@ -441,6 +487,21 @@ lcma_status make_map(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64_t co
     return LCMA_OK;
 }
 
+// Diagnostics only (LCMA_STATS set): a process-lifetime device buffer for the
+// per-CTA wait-cycle counters; read back with lcma_debug_stats().
+unsigned long long* g_stats = nullptr;
+unsigned long long* lcma_debug_stats_buffer() {
+    if (!g_stats) {
+        if (cudaMalloc(&g_stats, 1024 * 8 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaGetLastError();
+            g_stats = nullptr;
+        } else {
+            cudaMemset(g_stats, 0, 1024 * 8 * sizeof(unsigned long long));
+        }
+    }
+    return g_stats;
+}
+
 lcma_status check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -448,12 +509,13 @@ lcma_status check_launch(const char* what) {
     return LCMA_OK;
 }
 
+template <int CG>
 lcma_status ensure_smem_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kSmemBytes);
+        err = cudaFuncSetAttribute(umma_gemm_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Cfg<CG>::kSmemBytes);
     });
     if (err != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
     return LCMA_OK;
@@ -547,7 +609,7 @@ lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cuda
 // materialised At / Bt with the fused Combine H (or H store) epilogue.
 lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, void* C, float* P,
                         int* flags, float* H, cudaStream_t st) {
-    lcma_status rs = ensure_smem_attr();
+    lcma_status rs = p->cg == 2 ? ensure_smem_attr<2>() : ensure_smem_attr<1>();
     if (rs != LCMA_OK) return rs;
     const Scheme& S = p->sch;
     const bool classical = p->scheme_id == SCHEME_CLASSICAL;
@@ -563,7 +625,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     if (!b_mn) {   // N x K (K-major)
         const uint64_t cols = classical ? p->d.K : p->Kb;
         const uint64_t rows = classical ? p->d.N : (uint64_t)S.R * p->Nb;
-        rs = make_map(&tb, Bop, dt, cols, rows, epr, kBN);
+        rs = make_map(&tb, Bop, dt, cols, rows, epr, kBN / p->cg);
     } else {       // K x N (MN-major): boxes of 128 bytes of N x BK rows
         const uint64_t cols = classical ? p->d.N : p->Nb;
         const uint64_t rows = classical ? p->d.K : (uint64_t)S.R * p->Kb;
@@ -578,20 +640,47 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     g.b_rows_per_r = classical ? 0 : (int)(b_mn ? p->Kb : p->Nb);
     g.b_mn_major = b_mn;
     g.tf32 = dt == LCMA_TF32;
-    g.idesc = ptx::make_idesc(dt == LCMA_BF16 ? 1u : dt == LCMA_FP16 ? 0u : 2u, kBM, kBN, b_mn ? 1u : 0u, 0u);
-    g.W = p->ctas; g.q = p->q; g.tail_c = p->tail_c; g.swz = p->swz;
+    g.idesc = ptx::make_idesc(dt == LCMA_BF16 ? 1u : dt == LCMA_FP16 ? 0u : 2u, kBM * p->cg, kBN,
+                              b_mn ? 1u : 0u, 0u);
+    g.W = p->ctas / p->cg; g.q = p->q; g.tail_c = p->tail_c; g.swz = p->swz;
     g.epi_mode = H ? EPI_STORE_H : EPI_FUSED;
     g.out_type = (p->d.out_dtype == LCMA_FP32 || p->d.out_dtype == LCMA_TF32) ? OUT_FP32
                  : p->d.out_dtype == LCMA_BF16 ? OUT_BF16 : OUT_FP16;
     g.m = S.m; g.n = S.n;
     g.M = p->d.M; g.N = p->d.N; g.Mb = p->Mb; g.Nb = p->Nb; g.ldc = p->d.N;
     g.C = C; g.P = P; g.flags = flags; g.H = H;
+    if (const char* dbg = std::getenv("LCMA_DEBUG")) g.debug = std::atoi(dbg);
+    if (const char* ph = std::getenv("LCMA_PARTIAL_HINT")) g.partial_hint = std::atoi(ph);
+    if (const char* oh = std::getenv("LCMA_OPERAND_HINT")) g.operand_hint = std::atoi(oh);
+    if (const char* sw = std::getenv("LCMA_SWZ")) g.swz = std::max(1, std::atoi(sw));
+    if (std::getenv("LCMA_STATS")) g.stats = lcma_debug_stats_buffer();
     const int mn = S.m * S.n;
     if (S.R > kMaxR || mn > kMaxMN) return fail(LCMA_ERR_NOT_SUPPORTED, "scheme too large for the fused kernel");
     for (int r = 0; r < S.R; ++r)
         for (int ij = 0; ij < mn; ++ij) g.Wc[r * mn + ij] = S.W[(size_t)r * mn + ij];
-    umma_gemm_kernel<<<p->ctas, kThreads, kSmemBytes, st>>>(ta, tb, g);
-    return check_launch("umma_gemm_kernel");
+    if (t_ev_start) cudaEventRecord(t_ev_start, st);
+    if (p->cg == 1) {
+        umma_gemm_kernel<1><<<p->ctas, kThreads, Cfg<1>::kSmemBytes, st>>>(ta, tb, g);
+    } else {
+        cudaLaunchConfig_t cfg;
+        std::memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3(p->ctas);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = Cfg<2>::kSmemBytes;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2>, ta, tb, g);
+        if (e != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
+    }
+    lcma_status ls = check_launch("umma_gemm_kernel");
+    if (t_ev_end) cudaEventRecord(t_ev_end, st);
+    return ls;
 }
 
 lcma_status launch_simt(const lcma_plan_s* p, const float* A, const float* B, float* H,
@@ -674,6 +763,12 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
 
 }  // namespace
 
+// Copies the diagnostic counters (8 per CTA) to host memory; 0 on success.
+extern "C" int lcma_debug_stats(unsigned long long* host, int n) {
+    if (!g_stats) return -1;
+    return cudaMemcpy(host, g_stats, (size_t)n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -1;
+}
+
 extern "C" lcma_status lcma_gemm(lcma_plan_t p, const void* A, const void* B, void* C, void* ws,
                                  size_t ws_bytes, void* stream) {
     if (p && !B) return fail(LCMA_ERR_INVALID_VALUE, "null B");
@@ -695,4 +790,13 @@ extern "C" lcma_status lcma_precombine_b(lcma_plan_t p, const void* B, void* Bt,
         return fail(LCMA_ERR_MISALIGNED, "device pointers must be 16-byte aligned");
     if (p->scheme_id == SCHEME_CLASSICAL) return fail(LCMA_ERR_INVALID_VALUE, "classical plan has no Bt");
     return launch_combine(p, B, Bt, true, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Measurement hook: when set (non-NULL cudaEvent_t handles), every following
+// lcma_gemm* call on this thread records `ev_start` / `ev_end` on the call's
+// stream immediately before / after the tcgen05 GEMM kernel, so a caller can
+// time the dominant kernel live.  Pass NULLs to disable.
+extern "C" void lcma_set_kernel_events(void* ev_start, void* ev_end) {
+    t_ev_start = reinterpret_cast<cudaEvent_t>(ev_start);
+    t_ev_end = reinterpret_cast<cudaEvent_t>(ev_end);
 }

@@ -4,15 +4,21 @@
 // stage 3/4).  The classical GEMM ("standard GEMM") is
 // the same kernel with the trivial scheme <1,1,1;1>.
 //
-// Roles (one CTA per SM, 384 threads):
+// CG = 1: one CTA per SM computes 128 x 256 tiles (tcgen05.mma cta_group::1).
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes 256 x 256 tiles with
+//         tcgen05.mma.cta_group::2 issued by the leader CTA; each CTA stages
+//         its 128 rows of A and its 128 columns of B, so per-SM shared-memory
+//         and L2 operand traffic per MMA flop are halved for B.
+//
+// Roles per CTA (384 threads):
 //   warp 0      TMA producer: At_r[x, y] and Bt_r[y, z] tiles -> smem ring
-//   warp 1      MMA issuer: one thread issues tcgen05.mma into TMEM
+//   warp 1      MMA issuer (leader CTA only): one thread issues tcgen05.mma
 //   warp 2      TMEM allocator (512 columns = 2 fp32 accumulators of 256)
 //   warps 4-11  epilogue: TMEM -> registers -> (Combine H) -> global
 //
 // Work decomposition (Group-Parallel Optimization): a *group* is
-// the set {H_r[x,z]}_{r=1..R} of one output tile position (x,z); the CTA that
-// owns a group accumulates every C_{ij}[x,z] with W[r,i,j] != 0 on chip/L2 and
+// the set {H_r[x,z]}_{r=1..R} of one output tile position (x,z); the CTA (pair)
+// that owns a group accumulates every C_{ij}[x,z] with W[r,i,j] != 0 and
 // writes C once.  Scheduling: lockstep rounds of whole groups
 // (all CTAs on the same r at the same time: cache-aware), then the tail of
 // G mod W groups split at tile granularity over all CTAs (split-group); the
@@ -26,18 +32,24 @@
 
 namespace lcma {
 
-constexpr int kBM = 128;          // UMMA M (cta_group::1)
+constexpr int kBM = 128;          // rows per CTA (TMEM lanes)
 constexpr int kBN = 256;          // UMMA N = accumulator columns
-constexpr int kStages = 4;        // smem ring depth
 constexpr int kThreads = 384;     // 12 warps
 constexpr int kEpiWarp0 = 4;      // first epilogue warp
 constexpr int kEpiWarps = 8;
 constexpr int kMaxR = 128;
 constexpr int kMaxMN = 32;
-constexpr int kTileBytesA = kBM * 128;    // 128 rows x 128 bytes
-constexpr int kTileBytesB = kBN * 128;    // 256 rows(K-major) or 4x(BK x 128B)
-constexpr int kStageBytes = kTileBytesA + kTileBytesB;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+template <int CG>
+struct Cfg {
+    static constexpr int kTileM = kBM * CG;                  // rows per group tile
+    static constexpr int kBNc = kBN / CG;                    // B columns staged per CTA
+    static constexpr int kABytes = kBM * 128;                // 128 rows x 128 bytes
+    static constexpr int kBBytes = kBNc * 128;               // kBNc x 128 B (K-major) or chunks (MN-major)
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = CG == 1 ? 4 : 6;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
 
 enum EpiMode : int { EPI_FUSED = 0, EPI_STORE_H = 1 };
 enum OutType : int { OUT_BF16 = 0, OUT_FP16 = 1, OUT_FP32 = 2 };
@@ -45,7 +57,7 @@ enum UnitRole : int { ROLE_WHOLE = 0, ROLE_OWNER = 1, ROLE_CONTRIB = 2 };
 
 struct GemmParams {
     // problem / blocking
-    int nX, nZ;            // tiles per block along M, N: Mb/kBM, Nb/kBN
+    int nX, nZ;            // group tiles along M, N: Mb/kTileM, Nb/kBN
     int G;                 // groups = nX * nZ
     int R;                 // products per group
     int nK;                // k-blocks per product: Kb / BK
@@ -56,20 +68,24 @@ struct GemmParams {
     int tf32;              // kind::tf32 (else kind::f16)
     uint32_t idesc;        // instruction descriptor
     // schedule
-    int W;                 // CTAs
+    int W;                 // work units run in parallel (CTAs for CG=1, pairs for CG=2)
     int q;                 // lockstep rounds of whole groups
-    int tail_c;            // tile capacity per CTA in the split tail
+    int tail_c;            // tile capacity per unit in the split tail
     int swz;               // raster band height (tiles) for group -> (x, z)
     // epilogue
     int epi_mode;
     int out_type;
+    int debug;             // bit0: skip epilogue global traffic (mainloop timing only)
+    int partial_hint;      // 1: L2 evict_last policy on partial tiles
+    int operand_hint;      // 1: L2 evict_first on operand TMA loads, 2: evict_last
+    unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics)
     int m, n;              // scheme grid (C blocks)
     long long M, N;        // true C extents (crop)
     long long Mb, Nb;      // block extents: C_ij origin = (i*Mb, j*Nb)
     long long ldc;
     void* C;
-    float* P;              // partial tiles: [2W][m*n][kBN/4][kBM][4] fp32
-    int* flags;            // [W] split-segment ready flags
+    float* P;              // partial tiles: [2*ctas][m*n][kBN/4][kBM][4] fp32
+    int* flags;            // [ctas] split-segment ready flags
     float* H;              // EPI_STORE_H: H [R][Mb][Nb] fp32
     int8_t Wc[kMaxR * kMaxMN];   // W[r][i*n + j]
 };
@@ -79,12 +95,13 @@ struct Unit {
     int g, r0, r1, role;
 };
 
-// Enumerates the units of CTA `w` in processing order.  Every role of the
-// CTA (producer, MMA, epilogue) walks the same sequence.
+// Enumerates the units of work-unit slot `w` in processing order.  Every role
+// of the CTA (producer, MMA, epilogue) and both CTAs of a pair walk the same
+// sequence.
 struct UnitIter {
     const GemmParams& p;
     int w;
-    int idx;           // lockstep round index, then tail
+    int idx;             // lockstep round index, then tail
     long long t, t_end;  // tail tile cursor
     __device__ UnitIter(const GemmParams& p_, int w_) : p(p_), w(w_), idx(0) {
         long long Tt = (long long)(p.G - p.q * p.W) * p.R;
@@ -137,6 +154,18 @@ __device__ __forceinline__ float4 ld_cg_f4(const float* p) {
 __device__ __forceinline__ void st_cg_f4(float* p, float4 v) {
     __stcg(reinterpret_cast<float4*>(p), v);
 }
+// partial-tile accesses with an L2 cache policy (evict_last keeps the
+// group's C_ij partials resident while operand tiles stream through L2)
+__device__ __forceinline__ float4 ld_pol_f4(const float* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_pol_f4(float* p, float4 v, uint64_t pol) {
+    asm volatile("st.global.cg.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
 
 // Store 32 consecutive fp32 values of one C row segment (cols c0..c0+31),
 // cropping to N.  N is a multiple of 8 (TMA rule) so 8-element vectors are
@@ -182,15 +211,29 @@ __device__ __forceinline__ size_t partial_off(int row, int col4) {
     return ((size_t)col4 * kBM + row) * 4;
 }
 
+// mbarrier wait that accumulates the cycles spent waiting (diagnostics only)
+__device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
+    if (acc) {
+        long long t0 = clock64();
+        ptx::mbar_wait(bar, parity);
+        *acc += (unsigned long long)(clock64() - t0);
+    } else {
+        ptx::mbar_wait(bar, parity);
+    }
+}
+
 // ------------------------------------------------------------ the kernel
+template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ GemmParams p) {
+    using C_ = Cfg<CG>;
+    constexpr int kStages = C_::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * C_::kStageBytes);
     uint64_t* empty_bar = full_bar + kStages;
     uint64_t* tfull_bar = empty_bar + kStages;   // [2]
     uint64_t* tempty_bar = tfull_bar + 2;        // [2]
@@ -198,69 +241,96 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    long long clk_entry = clock64();
+    if (p.stats && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.stats[blockIdx.x * 8 + 6] = t;
+    }
+    const uint32_t rank = CG == 1 ? 0u : ptx::cluster_ctarank();
+    const bool leader = rank == 0;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmap_a);
         ptx::tma_prefetch_desc(&tmap_b);
         for (int s = 0; s < kStages; ++s) {
-            ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], 1);
+            ptx::mbar_init(&full_bar[s], 1);        // the leader's expect_tx arrival
+            ptx::mbar_init(&empty_bar[s], 1);       // one commit per stage
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull_bar[a], 1);
-            ptx::mbar_init(&tempty_bar[a], kEpiWarps);
+            ptx::mbar_init(&tempty_bar[a], kEpiWarps * CG);
         }
         ptx::fence_mbar_init();
     }
     if (warp == 2) {
-        ptx::tmem_alloc(tmem_slot, 512);
-        ptx::tmem_relinquish();
+        ptx::tmem_alloc<CG>(tmem_slot, 512);
+        ptx::tmem_relinquish<CG>();
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int w = blockIdx.x;
+    const int w = blockIdx.x / CG;           // work-unit slot (pair index for CG = 2)
 
     if (warp == 0) {
-        // ================================ TMA producer
+        // ================================ TMA producer (both CTAs of a pair)
         if (ptx::elect_one()) {
             const int b_bytes_chunk = p.BK * 128;   // MN-major chunk: BK rows x 128 B
-            const int n_chunks = kBN / p.BK;       // MN-major: 128-byte column chunks
+            const int n_chunks = C_::kBNc / p.BK;   // MN-major: 128-byte column chunks per CTA
             int stage = 0;
             uint32_t phase = 0;
+            unsigned long long w_empty = 0;
+            unsigned long long* st_empty = p.stats ? &w_empty : nullptr;
+            const uint64_t opol = p.operand_hint == 2 ? ptx::policy_evict_last() : ptx::policy_evict_first();
+            const bool ohint = p.operand_hint != 0;
             UnitIter it(p, w);
             Unit u;
             while (it.next(u)) {
                 int x, z;
                 group_xz(p, u.g, x, z);
                 for (int r = u.r0; r < u.r1; ++r) {
-                    const int a_row = r * p.a_rows_per_r + x * kBM;
+                    const int a_row = r * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
+                    const int b_col0 = z * kBN + (int)rank * C_::kBNc;
                     for (int kb = 0; kb < p.nK; ++kb) {
-                        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-                        uint8_t* sa = smem + stage * kStageBytes;
-                        uint8_t* sb = sa + kTileBytesA;
-                        ptx::mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
+                        timed_wait(&empty_bar[stage], phase ^ 1, st_empty);
+                        uint8_t* sa = smem + stage * C_::kStageBytes;
+                        uint8_t* sb = sa + C_::kABytes;
                         const int kcol = kb * p.BK;
-                        ptx::tma_load_2d(sa, &tmap_a, &full_bar[stage], kcol, a_row);
-                        if (!p.b_mn_major) {
-                            ptx::tma_load_2d(sb, &tmap_b, &full_bar[stage], kcol,
-                                             r * p.b_rows_per_r + z * kBN);
+                        if constexpr (CG == 1) {
+                            ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kStageBytes);
+                            ptx::tma_load_2d(sa, &tmap_a, &full_bar[stage], kcol, a_row);
+                            if (!p.b_mn_major) {
+                                ptx::tma_load_2d(sb, &tmap_b, &full_bar[stage], kcol, r * p.b_rows_per_r + b_col0);
+                            } else {
+                                for (int c = 0; c < n_chunks; ++c)
+                                    ptx::tma_load_2d(sb + c * b_bytes_chunk, &tmap_b, &full_bar[stage],
+                                                     b_col0 + c * p.BK, r * p.b_rows_per_r + kcol);
+                            }
                         } else {
-                            for (int c = 0; c < n_chunks; ++c)
-                                ptx::tma_load_2d(sb + c * b_bytes_chunk, &tmap_b, &full_bar[stage],
-                                                 z * kBN + c * p.BK,
-                                                 r * p.b_rows_per_r + kcol);
+                            // only the leader arms its barrier (with both CTAs' bytes);
+                            // the peer's TMA completes bytes on the leader's barrier
+                            const uint32_t lbar = ptx::mapa_shared(ptx::smem_u32(&full_bar[stage]), 0);
+                            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kStageBytes * CG);
+                            ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
+                            if (!p.b_mn_major) {
+                                ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol);
+                            } else {
+                                for (int c = 0; c < n_chunks; ++c)
+                                    ptx::tma_load_2d_cg2(sb + c * b_bytes_chunk, &tmap_b, lbar,
+                                                         b_col0 + c * p.BK, r * p.b_rows_per_r + kcol, ohint, opol);
+                            }
                         }
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
                 }
             }
+            if (p.stats) p.stats[blockIdx.x * 8 + 0] = w_empty;
         }
     } else if (warp == 1) {
-        // ================================ MMA issuer
-        if (ptx::elect_one()) {
+        // ================================ MMA issuer (leader CTA)
+        if (leader && ptx::elect_one()) {
             const int k_steps = 4;                        // BK / UMMA_K (32 bytes per step)
             const uint32_t b_lbo = p.BK * 128;            // MN-major: chunk stride
             const uint32_t b_kstep = p.b_mn_major ? (uint32_t)(32 / (p.tf32 ? 4 : 2)) * 128u : 32u;
@@ -268,18 +338,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            unsigned long long w_tempty = 0, w_full = 0;
+            const long long t_start = clock64();
             UnitIter it(p, w);
             Unit u;
             while (it.next(u)) {
                 for (int r = u.r0; r < u.r1; ++r) {
-                    ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+                    timed_wait(&tempty_bar[acc], acc_phase ^ 1, p.stats ? &w_tempty : nullptr);
                     ptx::tc_fence_after();
                     const uint32_t d_tmem = tmem_base + acc * kBN;
                     for (int kb = 0; kb < p.nK; ++kb) {
-                        ptx::mbar_wait(&full_bar[stage], phase);
+                        timed_wait(&full_bar[stage], phase, p.stats ? &w_full : nullptr);
                         ptx::tc_fence_after();
-                        const uint32_t sa = ptx::smem_u32(smem + stage * kStageBytes);
-                        const uint32_t sb = sa + kTileBytesA;
+                        const uint32_t sa = ptx::smem_u32(smem + stage * C_::kStageBytes);
+                        const uint32_t sb = sa + C_::kABytes;
 #pragma unroll
                         for (int ks = 0; ks < k_steps; ++ks) {
                             const uint64_t adesc = ptx::smem_desc_sw128(sa + ks * 32, 16, 1024);
@@ -287,26 +359,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 p.b_mn_major ? ptx::smem_desc_sw128(sb + ks * b_kstep, b_lbo, 1024)
                                              : ptx::smem_desc_sw128(sb + ks * 32, 16, 1024);
                             const uint32_t accum = (kb | ks) ? 1u : 0u;
-                            if (p.tf32)
-                                ptx::mma_tf32_ss(d_tmem, adesc, bdesc, p.idesc, accum);
-                            else
-                                ptx::mma_f16_ss(d_tmem, adesc, bdesc, p.idesc, accum);
+                            if constexpr (CG == 1) {
+                                if (p.tf32) ptx::mma_tf32_ss(d_tmem, adesc, bdesc, p.idesc, accum);
+                                else ptx::mma_f16_ss(d_tmem, adesc, bdesc, p.idesc, accum);
+                            } else {
+                                if (p.tf32) ptx::mma_tf32_ss_cg2(d_tmem, adesc, bdesc, p.idesc, accum);
+                                else ptx::mma_f16_ss_cg2(d_tmem, adesc, bdesc, p.idesc, accum);
+                            }
                         }
-                        ptx::mma_commit(&empty_bar[stage]);       // smem slot free when MMAs done
+                        // smem slot free (in both CTAs) once these MMAs completed
+                        if constexpr (CG == 1) ptx::mma_commit(&empty_bar[stage]);
+                        else ptx::mma_commit_cg2_mc(&empty_bar[stage], 0x3);
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
-                    ptx::mma_commit(&tfull_bar[acc]);             // accumulator ready
+                    // accumulator ready (in both CTAs)
+                    if constexpr (CG == 1) ptx::mma_commit(&tfull_bar[acc]);
+                    else ptx::mma_commit_cg2_mc(&tfull_bar[acc], 0x3);
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
             }
+            if (p.stats) {
+                p.stats[blockIdx.x * 8 + 1] = w_tempty;
+                p.stats[blockIdx.x * 8 + 2] = w_full;
+                p.stats[blockIdx.x * 8 + 3] = (unsigned long long)(clock64() - t_start);
+            }
         }
     } else if (warp >= kEpiWarp0) {
-        // ================================ epilogue
+        // ================================ epilogue (both CTAs: own 128 rows)
         const int ew = warp - kEpiWarp0;           // 0..7
         const int quarter = warp & 3;              // TMEM lane quarter
         const int half = ew >> 2;                  // column half
-        const int row = quarter * 32 + lane;       // tile row owned by this thread
+        const int row = quarter * 32 + lane;       // row of this CTA's 128-row slab
         const int mn = p.m * p.n;
+        const uint64_t pol = ptx::policy_evict_last();
+        unsigned long long w_tfull = 0;
+        const long long t_epi0 = clock64();
+        const uint32_t tempty_leader0 =
+            CG == 2 ? ptx::mapa_shared(ptx::smem_u32(&tempty_bar[0]), 0) : 0u;
         int acc = 0;
         uint32_t acc_phase = 0;
         UnitIter it(p, w);
@@ -314,6 +403,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (it.next(u)) {
             int x, z;
             group_xz(p, u.g, x, z);
+            // rows of this CTA inside the block grid
+            const long long brow = (long long)x * C_::kTileM + (long long)rank * kBM + row;
             // first / last contributing r of each C_ij inside this unit
             int first_r[kMaxMN], last_r[kMaxMN];
             for (int ij = 0; ij < mn; ++ij) {
@@ -325,9 +416,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         last_r[ij] = r;
                     }
             }
-            const int slot = (u.role == ROLE_CONTRIB) ? p.W + w : w;
+            const int slot = (u.role == ROLE_CONTRIB) ? (int)gridDim.x + (int)blockIdx.x : (int)blockIdx.x;
             for (int r = u.r0; r < u.r1; ++r) {
-                ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+                timed_wait(&tfull_bar[acc], acc_phase, (p.stats && ew == 0 && lane == 0) ? &w_tfull : nullptr);
                 ptx::tc_fence_after();
                 const uint32_t t_addr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
                                         (uint32_t)(acc * kBN + half * (kBN / 2));
@@ -340,13 +431,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         // all TMEM reads of this accumulator are done: release it
                         ptx::tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+                        if (lane == 0) {
+                            if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
+                            else ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+                        }
                     }
                     const int col0 = half * (kBN / 2) + ch * 32;   // column inside the tile
+                    if (p.debug & 1) continue;
                     if (p.epi_mode == EPI_STORE_H) {
                         // Algorithm 1 stage 3: H_r to main memory
-                        long long hr = (long long)x * kBM + row;
-                        float* dst = p.H + ((long long)r * p.Mb + hr) * p.Nb + (long long)z * kBN + col0;
+                        float* dst = p.H + ((long long)r * p.Mb + brow) * p.Nb + (long long)z * kBN + col0;
 #pragma unroll
                         for (int e = 0; e < 32; e += 4)
                             st_cg_f4(dst + e, make_float4(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1]),
@@ -365,49 +459,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (r != first_r[ij]) {
 #pragma unroll
                             for (int e = 0; e < 32; e += 4) {
-                                float4 o = ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
+                                float4 o = p.partial_hint ? ld_pol_f4(pt + partial_off(row, (col0 + e) >> 2), pol)
+                                                          : ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
                                 v[e] += o.x; v[e + 1] += o.y; v[e + 2] += o.z; v[e + 3] += o.w;
                             }
                         }
                         const bool final_here = (r == last_r[ij]) && (u.role == ROLE_WHOLE);
                         if (final_here) {
                             const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
-                            const long long crow = (long long)i * p.Mb + (long long)x * kBM + row;
                             const long long ccol = (long long)j * p.Nb + (long long)z * kBN + col0;
-                            // rows / cols beyond this block's extent belong to padding
-                            if ((long long)x * kBM + row < p.Mb && ccol < (long long)(j + 1) * p.Nb)
-                                store_c_row(p, crow, ccol, v);
+                            if (brow < p.Mb && ccol < (long long)(j + 1) * p.Nb)
+                                store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
                         } else {
 #pragma unroll
-                            for (int e = 0; e < 32; e += 4)
-                                st_cg_f4(pt + partial_off(row, (col0 + e) >> 2),
-                                         make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+                            for (int e = 0; e < 32; e += 4) {
+                                const float4 o = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                                if (p.partial_hint) st_pol_f4(pt + partial_off(row, (col0 + e) >> 2), o, pol);
+                                else st_cg_f4(pt + partial_off(row, (col0 + e) >> 2), o);
+                            }
                         }
                     }
                 }
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
-            if (p.epi_mode != EPI_FUSED || u.role == ROLE_WHOLE) continue;
+            if (p.epi_mode != EPI_FUSED || u.role == ROLE_WHOLE || (p.debug & 1)) continue;
 
             // ---- split group: publish (contributor) or merge (owner)
-            // named barrier over the 256 epilogue threads
             if (u.role == ROLE_CONTRIB) {
                 __threadfence();
                 asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
                 if (ew == 0 && lane == 0) {
-                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flags + w), "r"(1)
+                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flags + blockIdx.x), "r"(1)
                                  : "memory");
                 }
                 continue;
             }
-            // owner: segments live on CTAs w+1 .. last
+            // owner: the other segments live on work units w+1 .. last (same rank)
             const long long Tt_base = (long long)(u.g - p.q * p.W) * p.R;   // tail-local first tile
-            const int last_cta = (int)((Tt_base + p.R - 1) / p.tail_c);
+            const int last_w = (int)((Tt_base + p.R - 1) / p.tail_c);
             if (ew == 0 && lane == 0) {
-                for (int v = w + 1; v <= last_cta; ++v) {
+                for (int v = w + 1; v <= last_w; ++v) {
                     int f = 0;
                     do {
-                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.flags + v)
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.flags + v * CG + rank)
                                      : "memory");
                     } while (f == 0);
                 }
@@ -422,16 +516,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) v[e] = 0.f;
                     if (first_r[ij] >= 0) {
-                        const float* pt = partial_tile(p, w, ij);
+                        const float* pt = partial_tile(p, blockIdx.x, ij);
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
                             float4 o = ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
                             v[e] += o.x; v[e + 1] += o.y; v[e + 2] += o.z; v[e + 3] += o.w;
                         }
                     }
-                    for (int vcta = w + 1; vcta <= last_cta; ++vcta) {
-                        // does CTA vcta's segment contribute to C_ij?
-                        long long lo = (long long)vcta * p.tail_c - Tt_base;
+                    for (int vw = w + 1; vw <= last_w; ++vw) {
+                        // does unit vw's segment contribute to C_ij?
+                        long long lo = (long long)vw * p.tail_c - Tt_base;
                         long long hi = lo + p.tail_c;
                         if (lo < 0) lo = 0;
                         if (hi > p.R) hi = p.R;
@@ -439,31 +533,40 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (long long r = lo; r < hi; ++r)
                             if (p.Wc[r * mn + ij]) { contributes = true; break; }
                         if (!contributes) continue;
-                        const float* pt = partial_tile(p, p.W + vcta, ij);
+                        const float* pt = partial_tile(p, (int)gridDim.x + vw * CG + (int)rank, ij);
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
                             float4 o = ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
                             v[e] += o.x; v[e + 1] += o.y; v[e + 2] += o.z; v[e + 3] += o.w;
                         }
                     }
-                    const long long crow = (long long)i * p.Mb + (long long)x * kBM + row;
                     const long long ccol = (long long)j * p.Nb + (long long)z * kBN + col0;
-                    if ((long long)x * kBM + row < p.Mb && ccol < (long long)(j + 1) * p.Nb)
-                        store_c_row(p, crow, ccol, v);
+                    if (brow < p.Mb && ccol < (long long)(j + 1) * p.Nb)
+                        store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
                 }
             }
             // all reads done -> reset the flags for the next launch
             asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
             if (ew == 0 && lane == 0)
-                for (int v = w + 1; v <= last_cta; ++v) p.flags[v] = 0;
+                for (int v = w + 1; v <= last_w; ++v) p.flags[v * CG + rank] = 0;
+        }
+        if (p.stats && ew == 0 && lane == 0) {
+            p.stats[blockIdx.x * 8 + 4] = w_tfull;
+            (void)t_epi0;
         }
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, 512);
+        ptx::tmem_dealloc<CG>(tmem_base, 512);
+    }
+    if (p.stats && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.stats[blockIdx.x * 8 + 7] = t;
+        p.stats[blockIdx.x * 8 + 5] = (unsigned long long)(clock64() - clk_entry);
     }
 }
 

@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Exact mode: small-integer inputs, fp32 C -> bit-exact equality with the int64
+oracle (every intermediate < 2^21).  Float mode:
+the BASELINE.json normwise gates plus eps_rel against the oracle's
+dtype-faithful emulation at the plan's block extents.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2605_06057_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+L = pytest.importorskip("paper_2605_06057_b200")
+
+SCHEMES = {"strassen": O.strassen, "strassen2": O.strassen2, "laderman": O.laderman}
+INT_RANGE = {"classical": (-4, 4), "strassen": (-2, 2), "strassen2": (-1, 1), "laderman": (-1, 1)}
+
+
+def _b_dense(B, b_layout):
+    return B if b_layout == 0 else B.t()
+
+
+def _exact_case(M, N, K, algo, dtype=0, b_layout=0, variant="auto", **kw):
+    lo, hi = INT_RANGE[algo]
+    A, B = inputs.operands(M, N, K, dtype, M + 7, N + K, dist="int", b_layout=b_layout, lo=lo, hi=hi)
+    plan = L.Plan(M, N, K, dtype=dtype, algo=algo, out_dtype=L.FP32, b_layout=b_layout,
+                  variant=variant, **kw)
+    C = plan.gemm(A.cuda(), B.cuda()).cpu().numpy()
+    Ai = A.to(torch.int64).numpy()
+    Bi = _b_dense(B, b_layout).to(torch.int64).numpy()
+    ref = O.gemm_i64(Ai, Bi)
+    if algo != "classical":
+        # the method mirror at the GPU's block extents (Alg. 1, exact)
+        lc = O.lcma_i64(Ai, Bi, SCHEMES[algo](), extents=(plan.info["Mb"], plan.info["Kb"], plan.info["Nb"]))
+        assert np.array_equal(lc.C, ref)
+        assert np.abs(ref).max() < 2 ** 21
+    bad = np.argwhere(C != ref)
+    assert bad.size == 0, f"{len(bad)} mismatches, first {bad[:3].tolist()}"
+    return plan
+
+
+@pytest.mark.parametrize("b_layout", [0, 1])
+@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 128), (300, 264, 200),
+                                   (1000, 1048, 520), (2304, 2560, 1024)])
+def test_classical_exact_bf16(shape, b_layout):
+    _exact_case(*shape, "classical", b_layout=b_layout)
+
+
+@pytest.mark.parametrize("dtype", [1, 2])
+def test_classical_exact_fp16_tf32(dtype):
+    _exact_case(520, 776, 392, "classical", dtype=dtype)
+    _exact_case(520, 776, 392, "classical", dtype=dtype, b_layout=1)
+
+
+@pytest.mark.parametrize("variant", ["fused_h", "unfused"])
+@pytest.mark.parametrize("b_layout", [0, 1])
+@pytest.mark.parametrize("algo,shape", [
+    ("strassen", (512, 512, 512)), ("strassen", (300, 264, 200)), ("strassen", (1000, 1560, 776)),
+    ("strassen2", (1024, 1024, 512)), ("strassen2", (700, 1032, 264)),
+    ("laderman", (768, 1536, 384)), ("laderman", (1000, 808, 520))])
+def test_lcma_exact(algo, shape, b_layout, variant):
+    _exact_case(*shape, algo, b_layout=b_layout, variant=variant)
+
+
+@pytest.mark.parametrize("dtype", [1, 2])
+def test_lcma_exact_fp16_tf32(dtype):
+    _exact_case(512, 1024, 384, "strassen", dtype=dtype)
+    _exact_case(1000, 520, 392, "strassen", dtype=dtype, b_layout=1)
+
+
+@pytest.mark.parametrize("num_ctas,schedule", [(6, 0), (10, 0), (14, 2), (2, 0), (148, 2)])
+def test_split_groups_exact(num_ctas, schedule):
+    # forces tail groups split over several CTAs (segments merged by the owner)
+    plan = _exact_case(1536, 2304, 512, "strassen", num_ctas=num_ctas, schedule=schedule)
+    assert plan.info["split_groups"] > 0 or plan.info["groups"] % (plan.info["ctas"] // plan.info["cta_group"]) == 0
+    _exact_case(1024, 1536, 256, "laderman", num_ctas=num_ctas, schedule=schedule)
+
+
+def test_precombined_b_matches_oracle_intermediates():
+    # Combine B (Eq. 4) materialised by lcma_precombine_b == oracle Bt, bitwise
+    M, N, K = 520, 776, 392
+    for b_layout in (0, 1):
+        A, B = inputs.operands(M, N, K, 0, 3, 4, dist="int", b_layout=b_layout, lo=-2, hi=2)
+        plan = L.Plan(M, N, K, dtype=L.BF16, algo="strassen", out_dtype=L.FP32, b_layout=b_layout)
+        Bt = plan.precombine_b(B.cuda())
+        Mb, Nb, Kb = plan.info["Mb"], plan.info["Nb"], plan.info["Kb"]
+        lc = O.lcma_i64(A.to(torch.int64).numpy(), _b_dense(B, b_layout).to(torch.int64).numpy(),
+                        O.strassen(), extents=(Mb, Kb, Nb), intermediates=True)
+        g = Bt[: 7 * Kb * Nb * 2].view(torch.bfloat16).float().cpu().numpy()
+        g = g.reshape(7, Kb, Nb) if b_layout == 0 else g.reshape(7, Nb, Kb).transpose(0, 2, 1)
+        assert np.array_equal(g, lc.Bt.astype(np.float32))
+        # and the precombined GEMM equals the full one bitwise
+        Ad = A.cuda()
+        C1 = plan.gemm(Ad, B.cuda())
+        C2 = plan.gemm_precombined(Ad, Bt)
+        assert torch.equal(C1, C2)
+
+
+def _float_case(M, N, K, algo, dtype, dist="uniform", b_layout=0, variant="auto"):
+    A, B = inputs.operands(M, N, K, dtype, 31, 32, dist=dist, b_layout=b_layout)
+    plan = L.Plan(M, N, K, dtype=dtype, algo=algo, b_layout=b_layout, variant=variant)
+    C = plan.gemm(A.cuda(), B.cuda()).double().cpu().numpy()
+    Ad = A.double().numpy()
+    Bd = _b_dense(B, b_layout).double().numpy()
+    ref = O.gemm_f64(Ad, Bd)
+    e = O.eps_norm(C, ref, Ad, Bd)
+    er = O.eps_rel(C, ref)
+    fmt = {0: "bf16", 1: "fp16", 2: "tf32"}[dtype]
+    out_fmt = {0: "bf16", 1: "fp16", 2: "fp32"}[dtype]
+    if algo == "classical":
+        if dtype == 2:   # the MMA sees tf32 operands
+            emu = O.gemm_f64(O.round_to(Ad, "tf32"), O.round_to(Bd, "tf32"))
+        else:
+            emu = O.round_to(ref, out_fmt)
+    else:
+        emu = O.lcma_f64(Ad, Bd, SCHEMES[algo](), extents=(plan.info["Mb"], plan.info["Kb"], plan.info["Nb"]),
+                         fmt_in=fmt, fmt_out=out_fmt).C
+    er_emu = O.eps_rel(emu, ref)
+    return e, er, er_emu, O.freivalds(C, Ad, Bd)
+
+
+@pytest.mark.parametrize("algo", ["classical", "strassen", "strassen2", "laderman"])
+@pytest.mark.parametrize("dtype,gate", [(0, 2e-2), (1, 3e-3), (2, 3e-3)])
+@pytest.mark.parametrize("dist", ["uniform", "positive"])
+def test_float_tolerance(algo, dtype, gate, dist):
+    e, er, er_emu, fv = _float_case(1032, 1544, 1032, algo, dtype, dist=dist)
+    assert e <= gate
+    assert er <= 3.0 * er_emu + 1e-6, (er, er_emu)     # within 3x the dtype-faithful emulation
+    assert fv <= gate
+
+
+def test_fp32_cfg1_simt():
+    # cfg1: Strassen one level, 256^3, true fp32 (BASELINE gate 1e-5)
+    for algo in ("strassen", "classical"):
+        A, B = inputs.operands(256, 256, 256, L.FP32, 101, 102)
+        plan = L.Plan(256, 256, 256, dtype=L.FP32, algo=algo)
+        C = plan.gemm(A.cuda(), B.cuda()).double().cpu().numpy()
+        ref = O.gemm_f64(A.double().numpy(), B.double().numpy())
+        assert O.eps_norm(C, ref, A.double().numpy(), B.double().numpy()) <= 1e-5
+    _exact_case(256, 256, 256, "strassen", dtype=L.FP32)
+    _exact_case(300, 264, 200, "strassen2", dtype=L.FP32)
+
+
+def test_determinism_bitwise():
+    A, B = inputs.operands(1536, 2304, 1024, 0, 41, 42)
+    Ad, Bd = A.cuda(), B.cuda()
+    for algo in ("strassen", "laderman", "classical"):
+        plan = L.Plan(1536, 2304, 1024, dtype=L.BF16, algo=algo, num_ctas=20)
+        C1 = plan.gemm(Ad, Bd).clone()
+        for _ in range(3):
+            assert torch.equal(plan.gemm(Ad, Bd), C1)
+
+
+def test_cfg2_full_size_sampled():
+    # BASELINE cfg2 at full size in the bench configuration: sampled rows vs the
+    # fp64 oracle, Freivalds over all of C, and an exact-integer run.
+    M, N, K = 8192, 14336, 4096
+    A, B = inputs.operands(M, N, K, 0, 201, 202)
+    plan = L.Plan(M, N, K, dtype=L.BF16, algo="strassen")
+    C = plan.gemm(A.cuda(), B.cuda())
+    rng = np.random.default_rng(0)
+    Mb = plan.info["Mb"]
+    rows = np.unique(np.concatenate([rng.choice(M, 48, replace=False),
+                                     [0, 127, 128, 255, 256, Mb - 1, Mb, Mb + 1, M - 1]]))
+    Ad = A.double().numpy()
+    Bd = B.double().numpy()
+    ref = O.gemm_rows_f64(Ad, Bd, rows)
+    got = C[torch.from_numpy(rows).cuda()].double().cpu().numpy()
+    assert O.eps_rel(got, ref) < 1e-2
+    assert np.abs(got - ref).max() < 0.6
+    assert O.freivalds(C.double().cpu().numpy(), Ad, Bd, trials=2) < 2e-2
+    # exact integer mode at full size
+    Ai, Bi = inputs.operands(M, N, K, 0, 203, 204, dist="int", lo=-1, hi=1)
+    plan = L.Plan(M, N, K, dtype=L.BF16, algo="strassen", out_dtype=L.FP32)
+    Ci = plan.gemm(Ai.cuda(), Bi.cuda())
+    refi = O.gemm_rows_f64(Ai.double().numpy(), Bi.double().numpy(), rows)
+    assert np.array_equal(Ci[torch.from_numpy(rows).cuda()].double().cpu().numpy(), refi)
+
+
+def test_error_paths():
+    plan = L.Plan(256, 512, 256, dtype=L.BF16, algo="strassen")
+    A = torch.zeros(256 * 256 + 8, dtype=torch.bfloat16, device="cuda")
+    B = torch.zeros(256, 512, dtype=torch.bfloat16, device="cuda")
+    C = torch.empty(256, 512, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(L.LcmaError, match="MISALIGNED"):
+        plan.gemm(A[1:], B, C)
+    with pytest.raises(L.LcmaError, match="WORKSPACE"):
+        plan.gemm(A[:256 * 256], B, C, workspace=torch.zeros(16, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(L.LcmaError, match="INVALID"):
+        plan.gemm(A[:256 * 256], B, A[:256 * 512])
+    with pytest.raises(L.LcmaError, match="MISALIGNED"):
+        L.Plan(256, 500, 256, dtype=L.BF16)
+
+
+def test_fake_multi_gpu_block_rows():
+    # block-row partition on one GPU: shards planned independently, stacked == full
+    from paper_2605_06057_b200 import shard
+    M, N, K, P = 2048, 1024, 512, 4
+    A, B = inputs.operands(M, N, K, 0, 51, 52, dist="int", lo=-2, hi=2)
+    parts = []
+    for p in range(P):
+        r0, r1 = shard.row_block(M, P, p)
+        plan = L.Plan(r1 - r0, N, K, dtype=L.BF16, algo="strassen", out_dtype=L.FP32)
+        parts.append(plan.gemm(A[r0:r1].cuda(), B.cuda()).cpu())
+    C = torch.cat(parts).numpy()
+    assert np.array_equal(C, O.gemm_i64(A.to(torch.int64).numpy(), B.to(torch.int64).numpy()))

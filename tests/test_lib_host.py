@@ -1,0 +1,148 @@
+"""CPU tests of the C-ABI library's host side (no GPU): the library loads and
+exports every symbol include/lcma.h declares; its independently written
+scheme tables, decision model and schedule agree with the oracle."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_06057_b200 as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "lcma.h")).read()
+    names = set(re.findall(r"\b(lcma_[a-z_]+)\s*\(", hdr))
+    assert len(names) >= 18
+    lib = L.lib()
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+@pytest.mark.parametrize("sid,make", [(1, O.strassen), (2, O.strassen2), (3, O.laderman)])
+def test_library_tables_equal_oracle(sid, make):
+    m, k, n, R, U, V, W = L.scheme_get(sid)
+    s = make()
+    assert (m, k, n, R) == (s.m, s.k, s.n, s.R)
+    assert np.array_equal(U, s.U) and np.array_equal(V, s.V) and np.array_equal(W, s.W)
+    assert O.brent(O.Scheme("lib", m, k, n, U, V, W))[0] == 0
+
+
+def test_register_file_and_errors(tmp_path):
+    s = O.laderman()
+    p = tmp_path / "laderman.txt"
+    p.write_text(O.scheme_to_text(s))
+    sid = L.scheme_register_file(str(p))
+    m, k, n, R, U, V, W = L.scheme_get(sid)
+    assert np.array_equal(U, s.U) and np.array_equal(W, s.W)
+    # sign flip -> SCHEME_INVALID with the failing tuple in the message
+    W2 = s.W.copy()
+    W2[0][np.nonzero(W2[0])[0][0], np.nonzero(W2[0])[1][0]] *= -1
+    with pytest.raises(L.LcmaError, match="SCHEME_INVALID.*Brent"):
+        L.scheme_register(s.U, s.V, W2)
+    txt = O.scheme_to_text(O.strassen()).splitlines()
+    txt[2] = "2 0"
+    p.write_text("\n".join(txt))
+    with pytest.raises(L.LcmaError, match="COEFF_RANGE"):
+        L.scheme_register_file(str(p))
+    p.write_text("2 2 2\n")
+    with pytest.raises(L.LcmaError, match="PARSE.*line 1"):
+        L.scheme_register_file(str(p))
+    # registered scheme is usable by a plan
+    sid2 = L.scheme_register(O.strassen().U, O.strassen().V, O.strassen().W, "s-copy")
+    plan = L.Plan(512, 512, 512, algo="scheme", scheme_id=sid2)
+    assert plan.info["R"] == 7
+
+
+def test_decision_matches_oracle_random():
+    rng = np.random.default_rng(3)
+    cat = [O.strassen(), O.strassen2(), O.laderman()]
+    names = {1: "classical", 2: "strassen-2x2x2-r7", 3: "strassen2-4x4x4-r49", 4: "laderman-3x3x3-r23"}
+    for _ in range(200):
+        M, N, K = (int(v) for v in rng.integers(64, 40000, 3))
+        fm = 10 ** rng.uniform(12, 15.5)
+        beta = fm / 10 ** rng.uniform(0, 3.5)
+        fa = beta * 10 ** rng.uniform(-1, 1.5)
+        for fused in (True, False):
+            d = O.select(cat, M, N, K, O.Profile(fm, fa, beta), fused)
+            info = L.decide(M, N, K, L.BF16, hw={"flops_mul": fm, "flops_add": fa, "beta_elems": beta},
+                            fused=fused)
+            assert names[info["algo"]] == d.choice
+            assert info["t_pred_classical"] == pytest.approx(d.times["classical"], rel=1e-12)
+            assert info["t_pred_choice"] == pytest.approx(d.times[d.choice], rel=1e-12)
+            assert bool(info["memory_bound"]) == d.memory_bound
+
+
+def test_decision_crossover_and_flags():
+    hw = {"flops_mul": 100.0, "flops_add": 1.0, "beta_elems": 1.0}
+    for n, expect in ((4096, True), (1024, False)):
+        plan = L.Plan(n, n, n, algo="strassen", hw=hw)
+        assert bool(plan.info["fused_condition"]) == expect      # N/26 > 100
+    assert not L.Plan(64, 64, 64, hw=hw).info["lcma_condition"]
+
+
+def test_plan_validation():
+    with pytest.raises(L.LcmaError, match="INVALID"):
+        L.Plan(0, 256, 256)
+    with pytest.raises(L.LcmaError, match="MISALIGNED"):
+        L.Plan(256, 256, 100)
+    with pytest.raises(L.LcmaError, match="NOT_SUPPORTED"):
+        L.Plan(256, 256, 256, dtype=L.FP32, algo="strassen", variant="fused_h")
+    with pytest.raises(L.LcmaError, match="INVALID"):
+        L.Plan(256, 256, 256, algo="scheme", scheme_id=999)
+
+
+def test_plan_extents_and_workspace():
+    p = L.Plan(8192, 14336, 4096, algo="strassen")
+    i = p.info
+    assert (i["Mb"], i["Nb"], i["Kb"]) == (4096, 7168, 2048)          # ceil extents
+    assert i["Mb"] % i["BM"] == 0 and i["Nb"] % i["BN"] == 0 and i["Kb"] % i["BK"] == 0
+    assert i["btilde_bytes"] == 7 * 2048 * 7168 * 2
+    p2 = L.Plan(1000, 1048, 520, algo="laderman")
+    i2 = p2.info
+    assert 3 * i2["Mb"] >= 1000 and 3 * i2["Nb"] >= 1048 and 3 * i2["Kb"] >= 520
+    assert L.Plan(256, 256, 256, algo="classical").workspace_bytes == 0
+
+
+def _flatten(plan):
+    W = plan.info["ctas"] // plan.info["cta_group"]
+    per = []
+    for w in range(W):
+        items = []
+        for g, r0, r1, role in plan.schedule(w):
+            items += [(g, r) for r in range(r0, r1)]
+        per.append(items)
+    return per
+
+
+def test_schedule_paper_mode_equals_oracle():
+    # schedule=2 is the paper's contiguous split-group order
+    for (M, N, K, algo) in [(8192, 14336, 4096, "strassen"), (4096, 4096, 4096, "strassen"),
+                            (12288, 12288, 1024, "laderman")]:
+        plan = L.Plan(M, N, K, algo=algo, schedule=2)
+        W = plan.info["ctas"] // plan.info["cta_group"]
+        sim = O.plan_split_group(plan.info["groups"], plan.info["R"], W)
+        assert _flatten(plan) == sim.assignments
+        assert plan.info["waves"] == sim.waves and plan.info["group_waves"] == sim.group_waves
+
+
+def test_schedule_lockstep_mode_properties():
+    for (M, N, K, algo, ctas) in [(8192, 14336, 4096, "strassen", 0), (1536, 2304, 512, "strassen", 6),
+                                  (12288, 12288, 1024, "strassen2", 0), (2048, 3072, 512, "laderman", 10)]:
+        plan = L.Plan(M, N, K, algo=algo, num_ctas=ctas)
+        per = _flatten(plan)
+        G, R = plan.info["groups"], plan.info["R"]
+        items = sorted(x for a in per for x in a)
+        assert items == [(g, r) for g in range(G) for r in range(R)]       # completeness
+        assert max(len(a) for a in per) == plan.info["waves"]
+        assert plan.info["waves"] == -(-G * R // len(per))                 # split-group wave count
+        # lockstep rounds: every worker on the same r in each full-round wave
+        W = len(per)
+        q = G // W
+        for t in range(q * R):
+            assert len({a[t][1] for a in per}) == 1
+        assert O.r_alignment(per) >= O.r_alignment(O.plan_split_group(G, R, W).assignments)
