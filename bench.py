@@ -207,6 +207,10 @@ def run_ours(args):
     # ---- timed region: K steps, inputs (400 MB) larger than L2 (126 MB)
     k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in range(args.steps)]
+    for a, b in k_ev:          # torch creates the CUDA events lazily: materialise them
+        a.record(stream)
+        b.record(stream)
+    torch.cuda.synchronize()
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -341,8 +345,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--algo", default="strassen")
     ap.add_argument("--variant", default="auto")

@@ -367,11 +367,12 @@ def gemm_rows_f64(A: np.ndarray, B: np.ndarray, rows) -> np.ndarray:
 
 
 # ========================================================= Algorithm 1
-FMT = {None: 0, "fp64": 0, "bf16": 1, "fp16": 2, "tf32": 3, "fp32": 4}
+FMT = {None: 0, "fp64": 0, "bf16": 1, "fp16": 2, "tf32": 3, "fp32": 4, "tf32_rz": 5}
 
 
 def round_to(x: np.ndarray, fmt: str) -> np.ndarray:
-    """Round fp64 values to bf16/fp16 (RN-even), tf32 (RN-away) or fp32."""
+    """Round fp64 values to bf16/fp16 (RN-even), tf32 (RN-away), fp32, or
+    truncate to tf32 ("tf32_rz")."""
     y = np.array(x, np.float64, copy=True, order="C")
     lib().or_round_array(_p(y), y.size, FMT[fmt])
     return y

@@ -31,7 +31,17 @@
 /* ---------------------------------------------------------------- rounding */
 /* fmt: 0 = none (fp64), 1 = bf16 (RN-even), 2 = fp16 (RN-even, IEEE binary16
  * range incl. subnormals and overflow to inf), 3 = tf32 (round-to-nearest,
- * ties away: cvt.rna.tf32.f32), 4 = fp32 (RN-even). */
+ * ties away: cvt.rna.tf32.f32), 4 = fp32 (RN-even), 5 = tf32 truncation
+ * (round toward zero: how the tf32 MMA reads raw fp32 operands). */
+static double round_sig(double x, int sig_bits, int ties_away, int emin, int emax);
+static double trunc_sig(double x, int sig_bits)
+{
+    if (x == 0.0 || !isfinite(x)) return x;
+    int e;
+    double f = frexp(x, &e);
+    double scaled = ldexp(f, sig_bits);
+    return ldexp(trunc(scaled), e - sig_bits);
+}
 static double round_sig(double x, int sig_bits, int ties_away, int emin, int emax)
 {
     if (x == 0.0 || !isfinite(x)) return x;
@@ -64,6 +74,7 @@ double or_round(double x, int fmt)
     case 2: return round_sig(x, 11, 0, -14, 15);
     case 3: return round_sig(x, 11, 1, -126, 127);
     case 4: return round_sig(x, 24, 0, -126, 127);
+    case 5: return trunc_sig(x, 11);
     default: return x;
     }
 }

@@ -464,7 +464,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 lcma_status make_map(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64_t cols, uint64_t rows,
-                     uint32_t box_c, uint32_t box_r) {
+                     uint32_t box_c, uint32_t box_r,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     auto fn = encode_fn();
     if (!fn) return fail(LCMA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     CUtensorMapDataType t = dt == LCMA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -476,7 +477,7 @@ lcma_status make_map(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64_t co
     cuuint32_t box[2] = {box_c, box_r};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(m, t, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         char buf[160];
@@ -629,7 +630,12 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     } else {       // K x N (MN-major): boxes of 128 bytes of N x BK rows
         const uint64_t cols = classical ? p->d.N : p->Nb;
         const uint64_t rows = classical ? p->d.K : (uint64_t)S.R * p->Kb;
-        rs = make_map(&tb, Bop, dt, cols, rows, epr, p->BK);
+        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
+        if (dt == LCMA_TF32 || dt == LCMA_FP32) {
+            if (const char* v = std::getenv("LCMA_TF32_MN_SWZ")) swz = (CUtensorMapSwizzle)std::atoi(v);
+            else swz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+        }
+        rs = make_map(&tb, Bop, dt, cols, rows, epr, p->BK, swz);
     }
     if (rs != LCMA_OK) return rs;
 
@@ -639,6 +645,11 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     g.a_rows_per_r = classical ? 0 : (int)p->Mb;
     g.b_rows_per_r = classical ? 0 : (int)(b_mn ? p->Kb : p->Nb);
     g.b_mn_major = b_mn;
+    // MN-major 32-bit operands use the 128B_BASE32B layout (4-row swizzle atoms)
+    g.b_layout_type = (dt == LCMA_TF32) ? 1 : 2;
+    g.b_sbo = (dt == LCMA_TF32) ? 512 : 1024;
+    if (const char* v = std::getenv("LCMA_TF32_MN_LT")) g.b_layout_type = std::atoi(v);
+    if (const char* v = std::getenv("LCMA_TF32_MN_SBO")) g.b_sbo = std::atoi(v);
     g.tf32 = dt == LCMA_TF32;
     g.idesc = ptx::make_idesc(dt == LCMA_BF16 ? 1u : dt == LCMA_FP16 ? 0u : 2u, kBM * p->cg, kBN,
                               b_mn ? 1u : 0u, 0u);

@@ -78,6 +78,8 @@ struct GemmParams {
     int debug;             // bit0: skip epilogue global traffic (mainloop timing only)
     int partial_hint;      // 1: L2 evict_last policy on partial tiles
     int operand_hint;      // 1: L2 evict_first on operand TMA loads, 2: evict_last
+    int b_layout_type;     // UMMA smem layout of B (2 = SWIZZLE_128B, 1 = 128B_BASE32B)
+    int b_sbo;             // B stride byte offset (8-row (or 4-row) K group stride)
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics)
     int m, n;              // scheme grid (C blocks)
     long long M, N;        // true C extents (crop)
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int ks = 0; ks < k_steps; ++ks) {
                             const uint64_t adesc = ptx::smem_desc_sw128(sa + ks * 32, 16, 1024);
                             const uint64_t bdesc =
-                                p.b_mn_major ? ptx::smem_desc_sw128(sb + ks * b_kstep, b_lbo, 1024)
+                                p.b_mn_major ? ptx::smem_desc(sb + ks * b_kstep, b_lbo, p.b_sbo, p.b_layout_type)
                                              : ptx::smem_desc_sw128(sb + ks * 32, 16, 1024);
                             const uint32_t accum = (kb | ks) ? 1u : 0u;
                             if constexpr (CG == 1) {

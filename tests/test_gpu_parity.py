@@ -112,8 +112,8 @@ def _float_case(M, N, K, algo, dtype, dist="uniform", b_layout=0, variant="auto"
     fmt = {0: "bf16", 1: "fp16", 2: "tf32"}[dtype]
     out_fmt = {0: "bf16", 1: "fp16", 2: "fp32"}[dtype]
     if algo == "classical":
-        if dtype == 2:   # the MMA sees tf32 operands
-            emu = O.gemm_f64(O.round_to(Ad, "tf32"), O.round_to(Bd, "tf32"))
+        if dtype == 2:   # the tf32 MMA truncates raw fp32 operands (reading 7)
+            emu = O.gemm_f64(O.round_to(Ad, "tf32_rz"), O.round_to(Bd, "tf32_rz"))
         else:
             emu = O.round_to(ref, out_fmt)
     else:
@@ -171,7 +171,9 @@ def test_cfg2_full_size_sampled():
     ref = O.gemm_rows_f64(Ad, Bd, rows)
     got = C[torch.from_numpy(rows).cuda()].double().cpu().numpy()
     assert O.eps_rel(got, ref) < 1e-2
-    assert np.abs(got - ref).max() < 0.6
+    # componentwise |C - C_ref| / (|A||B|)_ij, (|A||B|) by the same oracle
+    absAB = O.gemm_rows_f64(np.abs(Ad), np.abs(Bd), rows)
+    assert (np.abs(got - ref) / absAB).max() < 4e-3
     assert O.freivalds(C.double().cpu().numpy(), Ad, Bd, trials=2) < 2e-2
     # exact integer mode at full size
     Ai, Bi = inputs.operands(M, N, K, 0, 203, 204, dist="int", lo=-1, hi=1)

@@ -51,6 +51,8 @@ def test_rounding_matches_torch_and_numpy():
     # tf32: 10 stored mantissa bits, ties away from zero (cvt.rna.tf32.f32)
     t = O.round_to(np.array([1 + 2.0 ** -11, 1 + 3 * 2.0 ** -11, -(1 + 2.0 ** -11), 1 + 2.0 ** -12]), "tf32")
     assert t.tolist() == [1 + 2.0 ** -10, 1 + 2 * 2.0 ** -10, -(1 + 2.0 ** -10), 1.0]
+    z = O.round_to(np.array([1 + 3 * 2.0 ** -11, -(1 + 2.0 ** -11), 1.9999999]), "tf32_rz")
+    assert z.tolist() == [1 + 2.0 ** -10, -1.0, 2 - 2.0 ** -10]
     assert np.array_equal(O.round_to(x32.astype(np.float64) * 1.0000001, "fp32"),
                           (x32.astype(np.float64) * 1.0000001).astype(np.float32).astype(np.float64))
 
