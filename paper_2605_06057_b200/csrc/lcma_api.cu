@@ -57,13 +57,13 @@ int max_active_pairs() {
         cached = 0;
         int dev = 0;
         if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
-        if (cudaFuncSetAttribute(umma_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg<2>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return; }
+        if (cudaFuncSetAttribute(umma_gemm_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg<2, 256>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return; }
         cudaLaunchConfig_t cfg;
         std::memset(&cfg, 0, sizeof(cfg));
         cfg.gridDim = dim3(2);
         cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = Cfg<2>::kSmemBytes;
+        cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
@@ -72,7 +72,7 @@ int max_active_pairs() {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, umma_gemm_kernel<2>, &cfg) == cudaSuccess) cached = n;
+        if (cudaOccupancyMaxActiveClusters(&n, umma_gemm_kernel<2, 256>, &cfg) == cudaSuccess) cached = n;
         else cudaGetLastError();
     });
     return cached;
@@ -90,7 +90,7 @@ struct lcma_plan_s {
     int64_t Mb, Nb, Kb;
     int BK, e;
     int nX, nZ, G, nK;
-    int ctas, cg, q, tail_c, swz;
+    int ctas, cg, bn, q, tail_c, swz;
     size_t off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
     lcma_plan_info info;
 };
@@ -246,19 +246,22 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             if (pairs > 0) p->ctas = std::min(p->ctas, 2 * pairs);
         }
         const int tileM = kBM * p->cg;
+        p->bn = kBN;
+        if (const char* e_bn = std::getenv("LCMA_BN")) p->bn = std::atoi(e_bn) == 128 ? 128 : 256;
+        const int BNp = p->bn;
         if (classical) {
             p->nX = (int)cdiv(d.M, tileM);
-            p->nZ = (int)cdiv(d.N, kBN);
+            p->nZ = (int)cdiv(d.N, BNp);
             p->nK = (int)cdiv(d.K, p->BK);
             p->Mb = (int64_t)p->nX * tileM;
-            p->Nb = (int64_t)p->nZ * kBN;
+            p->Nb = (int64_t)p->nZ * BNp;
             p->Kb = (int64_t)p->nK * p->BK;
         } else {
             p->Mb = roundup(cdiv(d.M, S.m), tileM);
-            p->Nb = roundup(cdiv(d.N, S.n), kBN);
+            p->Nb = roundup(cdiv(d.N, S.n), BNp);
             p->Kb = roundup(cdiv(d.K, S.k), p->BK);
             p->nX = (int)(p->Mb / tileM);
-            p->nZ = (int)(p->Nb / kBN);
+            p->nZ = (int)(p->Nb / BNp);
             p->nK = (int)(p->Kb / p->BK);
         }
         if ((long long)p->nX * p->nZ > INT32_MAX / 2 || S.R * p->Mb > INT32_MAX ||
@@ -277,7 +280,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     if (!classical) {
         if (d.dtype != LCMA_FP32 && variant == LCMA_VARIANT_FUSED_H) {
             p->off_P = off;
-            off = align256(off + (size_t)2 * p->ctas * mn * kBM * kBN * sizeof(float));
+            off = align256(off + (size_t)2 * p->ctas * mn * kBM * p->bn * sizeof(float));
             p->off_flags = off;
             off = align256(off + (size_t)p->ctas * sizeof(int));
         }
@@ -302,7 +305,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     std::snprintf(I.scheme, sizeof(I.scheme), "%s", S.name.c_str());
     I.Mb = p->Mb; I.Nb = p->Nb; I.Kb = p->Kb;
     I.BM = d.dtype == LCMA_FP32 ? 128 : kBM * p->cg;
-    I.BN = d.dtype == LCMA_FP32 ? 128 : kBN;
+    I.BN = d.dtype == LCMA_FP32 ? 128 : p->bn;
     I.BK = p->BK;
     I.cta_group = p->cg;
     I.t_pred_classical = dec.t_std;
@@ -510,13 +513,13 @@ lcma_status check_launch(const char* what) {
     return LCMA_OK;
 }
 
-template <int CG>
+template <int CG, int BN>
 lcma_status ensure_smem_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(umma_gemm_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   Cfg<CG>::kSmemBytes);
+        err = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Cfg<CG, BN>::kSmemBytes);
     });
     if (err != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
     return LCMA_OK;
@@ -610,7 +613,8 @@ lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cuda
 // materialised At / Bt with the fused Combine H (or H store) epilogue.
 lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, void* C, float* P,
                         int* flags, float* H, cudaStream_t st) {
-    lcma_status rs = p->cg == 2 ? ensure_smem_attr<2>() : ensure_smem_attr<1>();
+    lcma_status rs = p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>() : ensure_smem_attr<2, 256>())
+                                : (p->bn == 128 ? ensure_smem_attr<1, 128>() : ensure_smem_attr<1, 256>());
     if (rs != LCMA_OK) return rs;
     const Scheme& S = p->sch;
     const bool classical = p->scheme_id == SCHEME_CLASSICAL;
@@ -626,7 +630,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     if (!b_mn) {   // N x K (K-major)
         const uint64_t cols = classical ? p->d.K : p->Kb;
         const uint64_t rows = classical ? p->d.N : (uint64_t)S.R * p->Nb;
-        rs = make_map(&tb, Bop, dt, cols, rows, epr, kBN / p->cg);
+        rs = make_map(&tb, Bop, dt, cols, rows, epr, p->bn / p->cg);
     } else {       // K x N (MN-major): boxes of 128 bytes of N x BK rows
         const uint64_t cols = classical ? p->d.N : p->Nb;
         const uint64_t rows = classical ? p->d.K : (uint64_t)S.R * p->Kb;
@@ -651,7 +655,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     if (const char* v = std::getenv("LCMA_TF32_MN_LT")) g.b_layout_type = std::atoi(v);
     if (const char* v = std::getenv("LCMA_TF32_MN_SBO")) g.b_sbo = std::atoi(v);
     g.tf32 = dt == LCMA_TF32;
-    g.idesc = ptx::make_idesc(dt == LCMA_BF16 ? 1u : dt == LCMA_FP16 ? 0u : 2u, kBM * p->cg, kBN,
+    g.idesc = ptx::make_idesc(dt == LCMA_BF16 ? 1u : dt == LCMA_FP16 ? 0u : 2u, kBM * p->cg, p->bn,
                               b_mn ? 1u : 0u, 0u);
     g.W = p->ctas / p->cg; g.q = p->q; g.tail_c = p->tail_c; g.swz = p->swz;
     g.epi_mode = H ? EPI_STORE_H : EPI_FUSED;
@@ -670,25 +674,33 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     for (int r = 0; r < S.R; ++r)
         for (int ij = 0; ij < mn; ++ij) g.Wc[r * mn + ij] = S.W[(size_t)r * mn + ij];
     if (t_ev_start) cudaEventRecord(t_ev_start, st);
-    if (p->cg == 1) {
-        umma_gemm_kernel<1><<<p->ctas, kThreads, Cfg<1>::kSmemBytes, st>>>(ta, tb, g);
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(p->ctas);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p->cg;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = p->cg == 2 ? 1 : 0;
+    cudaError_t e;
+    if (p->cg == 2 && p->bn == 256) {
+        cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
+        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256>, ta, tb, g);
+    } else if (p->cg == 2) {
+        cfg.dynamicSmemBytes = Cfg<2, 128>::kSmemBytes;
+        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 128>, ta, tb, g);
+    } else if (p->bn == 256) {
+        cfg.dynamicSmemBytes = Cfg<1, 256>::kSmemBytes;
+        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<1, 256>, ta, tb, g);
     } else {
-        cudaLaunchConfig_t cfg;
-        std::memset(&cfg, 0, sizeof(cfg));
-        cfg.gridDim = dim3(p->ctas);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = Cfg<2>::kSmemBytes;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2>, ta, tb, g);
-        if (e != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
+        cfg.dynamicSmemBytes = Cfg<1, 128>::kSmemBytes;
+        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<1, 128>, ta, tb, g);
     }
+    if (e != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
     lcma_status ls = check_launch("umma_gemm_kernel");
     if (t_ev_end) cudaEventRecord(t_ev_end, st);
     return ls;

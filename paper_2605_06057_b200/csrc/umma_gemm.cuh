@@ -40,14 +40,14 @@ constexpr int kEpiWarps = 8;
 constexpr int kMaxR = 128;
 constexpr int kMaxMN = 32;
 
-template <int CG>
+template <int CG, int BN = kBN>
 struct Cfg {
     static constexpr int kTileM = kBM * CG;                  // rows per group tile
-    static constexpr int kBNc = kBN / CG;                    // B columns staged per CTA
+    static constexpr int kBNc = BN / CG;                     // B columns staged per CTA
     static constexpr int kABytes = kBM * 128;                // 128 rows x 128 bytes
     static constexpr int kBBytes = kBNc * 128;               // kBNc x 128 B (K-major) or chunks (MN-major)
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = CG == 1 ? 4 : 6;
+    static constexpr int kStages = (196608 / kStageBytes) > 8 ? 8 : (196608 / kStageBytes);
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -156,6 +156,14 @@ __device__ __forceinline__ float4 ld_cg_f4(const float* p) {
 __device__ __forceinline__ void st_cg_f4(float* p, float4 v) {
     __stcg(reinterpret_cast<float4*>(p), v);
 }
+// 16-byte fp32 reduction performed in L2 (REDG.E.ADD.F32x4): no data returns
+// to the SM, and operations of one thread on one address apply in order.
+__device__ __forceinline__ void red_add_f4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+// Store 8 consecutive fp32 values (cols c0..c0+7) of one C row, cropped.
+struct GemmParams;
 // partial-tile accesses with an L2 cache policy (evict_last keeps the
 // group's C_ij partials resident while operand tiles stream through L2)
 __device__ __forceinline__ float4 ld_pol_f4(const float* p, uint64_t pol) {
@@ -204,10 +212,35 @@ __device__ __forceinline__ void store_c_row(const GemmParams& p, long long row, 
     }
 }
 
+// Store 8 consecutive fp32 values (cols c0..c0+7) of one C row, cropped.
+__device__ __forceinline__ void store_c8(const GemmParams& p, long long row, long long c0, const float* v) {
+    if (row >= p.M || c0 >= p.N) return;
+    if (p.out_type == OUT_FP32) {
+        float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + c0;
+        *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+        uint32_t w4[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            if (p.out_type == OUT_BF16) {
+                __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+                w4[h] = *reinterpret_cast<uint32_t*>(&b);
+            } else {
+                __half2 b = __floats2half2_rn(v[2 * h], v[2 * h + 1]);
+                w4[h] = *reinterpret_cast<uint32_t*>(&b);
+            }
+        }
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.C) + row * p.ldc + c0) =
+            make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+}
+
 // Partial tile layout: [kBN/4][kBM][4] floats, so that the 32 threads of a
 // warp (32 consecutive rows) touch 512 contiguous bytes per float4 access.
+template <int BN = kBN>
 __device__ __forceinline__ float* partial_tile(const GemmParams& p, int slot, int ij) {
-    return p.P + ((size_t)slot * p.m * p.n + ij) * (size_t)(kBM * kBN);
+    return p.P + ((size_t)slot * p.m * p.n + ij) * (size_t)(kBM * BN);
 }
 __device__ __forceinline__ size_t partial_off(int row, int col4) {
     return ((size_t)col4 * kBM + row) * 4;
@@ -225,12 +258,12 @@ __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, unsig
 }
 
 // ------------------------------------------------------------ the kernel
-template <int CG>
+template <int CG, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ GemmParams p) {
-    using C_ = Cfg<CG>;
+    using C_ = Cfg<CG, BN>;
     constexpr int kStages = C_::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -294,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 group_xz(p, u.g, x, z);
                 for (int r = u.r0; r < u.r1; ++r) {
                     const int a_row = r * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
-                    const int b_col0 = z * kBN + (int)rank * C_::kBNc;
+                    const int b_col0 = z * BN + (int)rank * C_::kBNc;
                     for (int kb = 0; kb < p.nK; ++kb) {
                         timed_wait(&empty_bar[stage], phase ^ 1, st_empty);
                         uint8_t* sa = smem + stage * C_::kStageBytes;
@@ -348,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int r = u.r0; r < u.r1; ++r) {
                     timed_wait(&tempty_bar[acc], acc_phase ^ 1, p.stats ? &w_tempty : nullptr);
                     ptx::tc_fence_after();
-                    const uint32_t d_tmem = tmem_base + acc * kBN;
+                    const uint32_t d_tmem = tmem_base + acc * BN;
                     for (int kb = 0; kb < p.nK; ++kb) {
                         timed_wait(&full_bar[stage], phase, p.stats ? &w_full : nullptr);
                         ptx::tc_fence_after();
@@ -423,66 +456,74 @@ __global__ void __launch_bounds__(kThreads, 1)
                 timed_wait(&tfull_bar[acc], acc_phase, (p.stats && ew == 0 && lane == 0) ? &w_tfull : nullptr);
                 ptx::tc_fence_after();
                 const uint32_t t_addr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                                        (uint32_t)(acc * kBN + half * (kBN / 2));
-#pragma unroll 1
-                for (int ch = 0; ch < (kBN / 2) / 32; ++ch) {
-                    uint32_t raw[32];
-                    ptx::tmem_ld_32x32b_x32(t_addr + ch * 32, raw);
-                    ptx::tmem_wait_ld();
-                    if (ch == (kBN / 2) / 32 - 1) {
-                        // all TMEM reads of this accumulator are done: release it
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
-                            else ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
-                        }
-                    }
-                    const int col0 = half * (kBN / 2) + ch * 32;   // column inside the tile
-                    if (p.debug & 1) continue;
-                    if (p.epi_mode == EPI_STORE_H) {
-                        // Algorithm 1 stage 3: H_r to main memory
-                        float* dst = p.H + ((long long)r * p.Mb + brow) * p.Nb + (long long)z * kBN + col0;
+                                        (uint32_t)(acc * BN + half * (BN / 2));
+                // drain this thread's 128 accumulator columns, then release the
+                // accumulator to the MMA warp before any global-memory traffic
+                uint32_t raw[BN / 2];
 #pragma unroll
-                        for (int e = 0; e < 32; e += 4)
-                            st_cg_f4(dst + e, make_float4(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1]),
-                                                          __uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])));
-                        continue;
-                    }
-                    // Combine H (Eq. 6): C_ij += W[r,i,j] * H_r for every nonzero W
-                    for (int ij = 0; ij < mn; ++ij) {
-                        const int wc = p.Wc[r * mn + ij];
-                        if (!wc) continue;
-                        const float sw = (float)wc;
-                        float v[32];
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) v[e] = sw * __uint_as_float(raw[e]);
-                        float* pt = partial_tile(p, slot, ij);
-                        if (r != first_r[ij]) {
-#pragma unroll
-                            for (int e = 0; e < 32; e += 4) {
-                                float4 o = p.partial_hint ? ld_pol_f4(pt + partial_off(row, (col0 + e) >> 2), pol)
-                                                          : ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
-                                v[e] += o.x; v[e + 1] += o.y; v[e + 2] += o.z; v[e + 3] += o.w;
-                            }
-                        }
-                        const bool final_here = (r == last_r[ij]) && (u.role == ROLE_WHOLE);
-                        if (final_here) {
-                            const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
-                            const long long ccol = (long long)j * p.Nb + (long long)z * kBN + col0;
-                            if (brow < p.Mb && ccol < (long long)(j + 1) * p.Nb)
-                                store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 32; e += 4) {
-                                const float4 o = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-                                if (p.partial_hint) st_pol_f4(pt + partial_off(row, (col0 + e) >> 2), o, pol);
-                                else st_cg_f4(pt + partial_off(row, (col0 + e) >> 2), o);
-                            }
-                        }
-                    }
+                for (int ch = 0; ch < (BN / 2) / 32; ++ch)
+                    ptx::tmem_ld_32x32b_x32(t_addr + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(&raw[ch * 32]));
+                ptx::tmem_wait_ld();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
+                    else ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
                 }
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (p.debug & 1) continue;
+                const int col_base = half * (BN / 2);
+                if (p.epi_mode == EPI_STORE_H) {
+                    // Algorithm 1 stage 3: H_r to main memory
+                    float* dst = p.H + ((long long)r * p.Mb + brow) * p.Nb + (long long)z * BN + col_base;
+#pragma unroll
+                    for (int e = 0; e < BN / 2; e += 4)
+                        st_cg_f4(dst + e, make_float4(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1]),
+                                                      __uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])));
+                    continue;
+                }
+                // Combine H (Eq. 6): C_ij += W[r,i,j] * H_r for every nonzero W
+                for (int ij = 0; ij < mn; ++ij) {
+                    const int wc = p.Wc[r * mn + ij];
+                    if (!wc) continue;
+                    const float sw = (float)wc;
+                    float* pt = partial_tile<BN>(p, slot, ij);
+                    const bool first = (r == first_r[ij]);
+                    const bool final_here = (r == last_r[ij]) && (u.role == ROLE_WHOLE);
+                    if (final_here) {
+                        // last contribution: C_ij = partial + w*H_r, rounded once
+                        const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
+                        const long long ccol = (long long)j * p.Nb + (long long)z * BN + col_base;
+                        if (!(brow < p.Mb && ccol < (long long)(j + 1) * p.Nb)) continue;
+#pragma unroll
+                        for (int e = 0; e < BN / 2; e += 8) {
+                            float v[8];
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) v[t] = sw * __uint_as_float(raw[e + t]);
+                            if (!first) {
+                                const float4 o0 = ld_cg_f4(pt + partial_off(row, (col_base + e) >> 2));
+                                const float4 o1 = ld_cg_f4(pt + partial_off(row, (col_base + e + 4) >> 2));
+                                v[0] += o0.x; v[1] += o0.y; v[2] += o0.z; v[3] += o0.w;
+                                v[4] += o1.x; v[5] += o1.y; v[6] += o1.z; v[7] += o1.w;
+                            }
+                            store_c8(p, (long long)i * p.Mb + brow, ccol + e, v);
+                        }
+                    } else if (first) {
+#pragma unroll
+                        for (int e = 0; e < BN / 2; e += 4)
+                            st_cg_f4(pt + partial_off(row, (col_base + e) >> 2),
+                                     make_float4(sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
+                                                 sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3])));
+                    } else {
+                        // middle contribution: fire-and-forget L2 reduction (same
+                        // thread, same address => applied in program order)
+#pragma unroll
+                        for (int e = 0; e < BN / 2; e += 4)
+                            red_add_f4(pt + partial_off(row, (col_base + e) >> 2),
+                                       sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
+                                       sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3]));
+                    }
+                }
             }
             if (p.epi_mode != EPI_FUSED || u.role == ROLE_WHOLE || (p.debug & 1)) continue;
 
@@ -512,13 +553,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ij = 0; ij < mn; ++ij) {
                 const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
 #pragma unroll 1
-                for (int ch = 0; ch < (kBN / 2) / 32; ++ch) {
-                    const int col0 = half * (kBN / 2) + ch * 32;
+                for (int ch = 0; ch < (BN / 2) / 32; ++ch) {
+                    const int col0 = half * (BN / 2) + ch * 32;
                     float v[32];
 #pragma unroll
                     for (int e = 0; e < 32; ++e) v[e] = 0.f;
                     if (first_r[ij] >= 0) {
-                        const float* pt = partial_tile(p, blockIdx.x, ij);
+                        const float* pt = partial_tile<BN>(p, blockIdx.x, ij);
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
                             float4 o = ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
@@ -535,14 +576,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (long long r = lo; r < hi; ++r)
                             if (p.Wc[r * mn + ij]) { contributes = true; break; }
                         if (!contributes) continue;
-                        const float* pt = partial_tile(p, (int)gridDim.x + vw * CG + (int)rank, ij);
+                        const float* pt = partial_tile<BN>(p, (int)gridDim.x + vw * CG + (int)rank, ij);
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
                             float4 o = ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
                             v[e] += o.x; v[e + 1] += o.y; v[e + 2] += o.z; v[e + 3] += o.w;
                         }
                     }
-                    const long long ccol = (long long)j * p.Nb + (long long)z * kBN + col0;
+                    const long long ccol = (long long)j * p.Nb + (long long)z * BN + col0;
                     if (brow < p.Mb && ccol < (long long)(j + 1) * p.Nb)
                         store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
                 }
