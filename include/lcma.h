@@ -100,6 +100,9 @@ typedef struct {
                                  2 paper's contiguous split-group order           */
     int32_t num_ctas;         /* 0 = one per SM                                    */
     const lcma_hw_profile* hw;/* NULL -> built-in B200 profile                     */
+    int32_t decision_model;   /* algo AUTO: 0 = this build's B200-calibrated model
+                                 (reading 19), 1 = the paper's model
+                                 verbatim (as lcma_decide)              */
 } lcma_plan_desc;
 
 typedef struct {

@@ -41,7 +41,7 @@ class PlanDesc(ctypes.Structure):
                 ("scheme_id", ctypes.c_int32), ("b_layout", ctypes.c_int32),
                 ("b_static", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("schedule", ctypes.c_int32), ("num_ctas", ctypes.c_int32),
-                ("hw", ctypes.POINTER(HwProfile))]
+                ("hw", ctypes.POINTER(HwProfile)), ("decision_model", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -137,7 +137,8 @@ class Plan:
     """lcma_plan_ex wrapper.  gemm() takes CUDA torch tensors (row-major)."""
 
     def __init__(self, M, N, K, dtype=BF16, algo="auto", out_dtype=None, b_layout=0,
-                 variant="auto", b_static=False, schedule=0, num_ctas=0, scheme_id=0, hw=None):
+                 variant="auto", b_static=False, schedule=0, num_ctas=0, scheme_id=0, hw=None,
+                 decision_model=0):
         L = lib()
         if out_dtype is None:
             out_dtype = FP32 if dtype == TF32 else dtype
@@ -145,7 +146,7 @@ class Plan:
         d = PlanDesc(M, N, K, dtype, out_dtype, ALGO[algo] if isinstance(algo, str) else algo,
                      scheme_id, b_layout, int(b_static),
                      VARIANT[variant] if isinstance(variant, str) else variant,
-                     schedule, num_ctas, self._hw)
+                     schedule, num_ctas, self._hw, decision_model)
         h = ctypes.c_void_p()
         _check(L.lcma_plan_ex(ctypes.byref(d), ctypes.byref(h)))
         self._h = h

@@ -67,6 +67,62 @@ double condition_lhs(const Scheme& s, double M, double N, double K, bool fused) 
     return num / den;
 }
 
+// B200-calibrated model of this build's kernels (reading 14/19).
+// Same structure as the paper's (per-stage times summed, Table row flops /
+// elements), with the measured constants of this implementation:
+//  * Combine A / B run at the combine kernels' measured element rate
+//    beta_combine (they are HBM-latency bound, not at copy bandwidth);
+//  * the GEMM stage runs at the measured classical-kernel throughput FLOPS_x
+//    on the tile-rounded extents;
+//  * the fused Combine H (C_ij partials in L2) slows the mainloop by
+//    alpha * rho^2, rho = (partial bytes written/read per product) /
+//    (operand bytes loaded per product) -- fitted on Strassen, Laderman and
+//    Strassen^2 at cfg2 (profiles/); the unfused variant instead pays an
+//    HBM pass over H (R*Mb*Nb*4 + M*N*e bytes) at beta.
+double estimate_time_b200(const Scheme& s, double M, double N, double K, const Profile& hw,
+                          bool fused, bool b_static, double elem_bytes) {
+    const double R = s.R;
+    const double tileM = 256.0, tileN = 256.0, BK = 128.0 / elem_bytes;
+    const double Mb = std::ceil(std::ceil(M / s.m) / tileM) * tileM;
+    const double Nb = std::ceil(std::ceil(N / s.n) / tileN) * tileN;
+    const double Kb = std::ceil(std::ceil(K / s.k) / BK) * BK;
+    double t = 0.0;
+    t += (M * K + R * Mb * Kb) / hw.beta_combine;                       // Combine A
+    if (!b_static) t += (K * N + R * Kb * Nb) / hw.beta_combine;        // Combine B
+    const double t_mma = 2.0 * R * Mb * Nb * Kb / hw.flops_mul;         // R sub-GEMMs
+    if (fused) {
+        const double contrib = (double)s.nnzW() / R;                     // C_ij updates per product
+        const double partial = contrib * 128.0 * tileN * 4.0;           // fp32 partial bytes per CTA
+        const double operand = (Kb / BK) * (128.0 * 128.0 + 128.0 * 128.0);   // A + B half per CTA
+        const double rho = partial / operand;
+        t += t_mma * (1.0 + hw.alpha_partial * rho * rho);
+    } else {
+        t += t_mma + (R * Mb * Nb * 4.0 + M * N * elem_bytes) / (hw.beta * elem_bytes);
+    }
+    return t;
+}
+
+DecisionResult decide_b200(const std::vector<int>& ids, double M, double N, double K, const Profile& hw,
+                           bool fused, bool b_static, double elem_bytes) {
+    DecisionResult d;
+    d.scheme_id = SCHEME_CLASSICAL;
+    d.t_std = estimate_time_std(M, N, K, hw);
+    d.t_choice = d.t_std;
+    d.memory_bound = gemm_intensity(M, N, K) <= hw.flops_mul / hw.beta;
+    if (d.memory_bound) return d;
+    for (int id : ids) {
+        const Scheme* s = scheme_get(id);
+        if (!s || s->R >= s->m * s->k * s->n) continue;
+        const double t = estimate_time_b200(*s, M, N, K, hw, fused, b_static, elem_bytes);
+        d.candidates.emplace_back(id, t);
+        if (t < d.t_choice) {
+            d.t_choice = t;
+            d.scheme_id = id;
+        }
+    }
+    return d;
+}
+
 DecisionResult decide(const std::vector<int>& ids, double M, double N, double K, const Profile& hw,
                       bool fused, bool b_static) {
     DecisionResult d;
@@ -94,13 +150,19 @@ Profile default_profile(int dtype) {
     // FADD issue rate 148 SMs x 128 lanes x ~1.3 GHz sustained.
     Profile p;
     const double bytes = (dtype == 0 || dtype == 1) ? 2.0 : 4.0;
-    p.flops_mul = dtype <= 1 ? 1.39e15 : (dtype == 2 ? 0.69e15 : 60e12);
+    // classical tcgen05 kernel of this build, cfg2 (profiles/): 1.366 PF/s bf16
+    p.flops_mul = dtype <= 1 ? 1.366e15 : (dtype == 2 ? 0.66e15 : 60e12);
     p.flops_add = 148.0 * 128.0 * 1.3e9;
     p.beta = 6.55e12 / bytes;
+    // group_combine_kernel measured ~4.4 TB/s of read+write traffic (cfg2)
+    p.beta_combine = 4.4e12 / bytes;
+    // fused Combine-H mainloop slowdown coefficient (fit: Strassen 0.276 at
+    // rho 0.214, Laderman 1.08 at 0.404, Strassen^2 2.39 at 0.735)
+    p.alpha_partial = 6.0;
     if (const char* env = std::getenv("LCMA_PROFILE")) {
-        const char* keys[3] = {"flops_mul=", "flops_add=", "beta_elems="};
-        double* dst[3] = {&p.flops_mul, &p.flops_add, &p.beta};
-        for (int i = 0; i < 3; ++i) {
+        const char* keys[5] = {"flops_mul=", "flops_add=", "beta_elems=", "beta_combine=", "alpha_partial="};
+        double* dst[5] = {&p.flops_mul, &p.flops_add, &p.beta, &p.beta_combine, &p.alpha_partial};
+        for (int i = 0; i < 5; ++i) {
             const char* f = std::strstr(env, keys[i]);
             if (f) {
                 double v = std::atof(f + std::strlen(keys[i]));

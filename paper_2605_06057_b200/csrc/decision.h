@@ -13,6 +13,9 @@ struct Profile {
     double flops_mul;   // FLOPS_x: GEMM-stage throughput
     double flops_add;   // FLOPS_+: combine add/sub throughput
     double beta;        // off-chip bandwidth, elements/s of the dtype
+    // B200-calibrated model only (decide_b200):
+    double beta_combine = 0.0;    // combine kernels' element rate (elements/s)
+    double alpha_partial = 0.0;   // fused Combine-H mainloop slowdown coefficient
 };
 
 struct StageCost {
@@ -42,6 +45,13 @@ struct DecisionResult {
 // {classical} U candidates; ties -> classical, then lower id.
 DecisionResult decide(const std::vector<int>& candidate_ids, double M, double N, double K,
                       const Profile& hw, bool fused, bool b_static);
+
+// The same selection with this build's calibrated B200 cost model (see
+// decision.cpp); elem_bytes = storage bytes of the dtype.
+double estimate_time_b200(const Scheme& s, double M, double N, double K, const Profile& hw, bool fused,
+                          bool b_static, double elem_bytes);
+DecisionResult decide_b200(const std::vector<int>& candidate_ids, double M, double N, double K,
+                           const Profile& hw, bool fused, bool b_static, double elem_bytes);
 
 // Built-in B200 profile per dtype (0 bf16, 1 fp16, 2 tf32, 3 fp32), overridable
 // through the environment variable LCMA_PROFILE="flops_mul=..,flops_add=..,beta_elems=..".

@@ -180,8 +180,19 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     // ---- Decision Module; reported even when algo is forced
     const bool fused_model = d.variant != LCMA_VARIANT_UNFUSED && d.dtype != LCMA_FP32;
     std::vector<int> cands = {SCHEME_STRASSEN, SCHEME_STRASSEN2, SCHEME_LADERMAN};
-    DecisionResult dec = decide(cands, (double)d.M, (double)d.N, (double)d.K, p->hw, fused_model,
-                                d.b_static != 0);
+    // decision_model 0: this build's calibrated B200 model; 1: the paper's model verbatim
+    const bool paper_model = d.decision_model == 1;
+    if (!paper_model && !d.hw) {
+        if (p->hw.beta_combine <= 0) p->hw.beta_combine = p->hw.beta;
+    } else if (!paper_model) {
+        Profile def = default_profile((int)d.dtype);
+        p->hw.beta_combine = def.beta_combine * (p->hw.beta / def.beta);
+        p->hw.alpha_partial = def.alpha_partial;
+    }
+    DecisionResult dec = paper_model
+        ? decide(cands, (double)d.M, (double)d.N, (double)d.K, p->hw, fused_model, d.b_static != 0)
+        : decide_b200(cands, (double)d.M, (double)d.N, (double)d.K, p->hw, fused_model, d.b_static != 0,
+                      (double)e);
     switch (d.algo) {
         case LCMA_ALGO_AUTO: p->scheme_id = dec.scheme_id; break;
         case LCMA_ALGO_CLASSICAL: p->scheme_id = SCHEME_CLASSICAL; break;
@@ -312,8 +323,11 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     if (classical) {
         I.t_pred_choice = dec.t_std;
     } else {
-        I.t_pred_choice = estimate_time(S, (double)d.M, (double)d.N, (double)d.K, p->hw,
-                                        variant != LCMA_VARIANT_UNFUSED, d.b_static != 0);
+        I.t_pred_choice = paper_model
+            ? estimate_time(S, (double)d.M, (double)d.N, (double)d.K, p->hw, variant != LCMA_VARIANT_UNFUSED,
+                            d.b_static != 0)
+            : estimate_time_b200(S, (double)d.M, (double)d.N, (double)d.K, p->hw,
+                                 variant != LCMA_VARIANT_UNFUSED, d.b_static != 0, (double)e);
     }
     I.speedup_pred = I.t_pred_classical / I.t_pred_choice;
     I.memory_bound = dec.memory_bound;
@@ -673,6 +687,20 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     if (S.R > kMaxR || mn > kMaxMN) return fail(LCMA_ERR_NOT_SUPPORTED, "scheme too large for the fused kernel");
     for (int r = 0; r < S.R; ++r)
         for (int ij = 0; ij < mn; ++ij) g.Wc[r * mn + ij] = S.W[(size_t)r * mn + ij];
+    // product order inside a group + shared partial slots (fused Combine H)
+    const bool use_order = !std::getenv("LCMA_ORDER") || std::atoi(std::getenv("LCMA_ORDER")) != 0;
+    if (use_order && !classical) {
+        const ProductOrder& po = scheme_product_order(p->scheme_id);
+        for (int t = 0; t < S.R; ++t) g.rperm[t] = (int8_t)po.perm[t];
+        for (int ij = 0; ij < mn; ++ij) g.pslot[ij] = (int8_t)po.slot[ij];
+        g.nslot = po.nslot;
+    } else {
+        for (int t = 0; t < S.R; ++t) g.rperm[t] = (int8_t)t;
+        for (int ij = 0; ij < mn; ++ij) g.pslot[ij] = (int8_t)ij;
+        g.nslot = mn;
+    }
+    g.discard = 1;
+    if (const char* dc = std::getenv("LCMA_DISCARD")) g.discard = std::atoi(dc);
     if (t_ev_start) cudaEventRecord(t_ev_start, st);
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));

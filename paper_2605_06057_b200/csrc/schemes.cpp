@@ -4,7 +4,9 @@
 // check the two against each other and against the Brent identity.
 #include "schemes.h"
 
+#include <algorithm>
 #include <cstdlib>
+#include <memory>
 #include <mutex>
 #include <sstream>
 
@@ -286,6 +288,121 @@ int scheme_parse(const std::string& text, Scheme& out, std::string& err) {
     }
     if (pos != lines.size()) return fail(lines[pos].first, "trailing content");
     return 0;
+}
+
+}  // namespace lcma
+
+// ------------------------------------------------------------ product order
+namespace lcma {
+namespace {
+
+struct OrderCost {
+    int max_live;
+    long long total_live;
+    bool operator<(const OrderCost& o) const {
+        return max_live != o.max_live ? max_live < o.max_live : total_live < o.total_live;
+    }
+};
+
+// Live range of C_ij = [first position contributing, last position contributing].
+OrderCost order_cost(const Scheme& s, const std::vector<int>& perm) {
+    const int mn = s.m * s.n, R = s.R;
+    std::vector<int> first(mn, -1), last(mn, -1);
+    for (int t = 0; t < R; ++t)
+        for (int ij = 0; ij < mn; ++ij)
+            if (s.W[(size_t)perm[t] * mn + ij]) {
+                if (first[ij] < 0) first[ij] = t;
+                last[ij] = t;
+            }
+    OrderCost c{0, 0};
+    for (int t = 0; t < R; ++t) {
+        int live = 0;
+        for (int ij = 0; ij < mn; ++ij) live += (first[ij] >= 0 && first[ij] <= t && t <= last[ij]);
+        c.max_live = std::max(c.max_live, live);
+        c.total_live += live;
+    }
+    return c;
+}
+
+ProductOrder compute_order(const Scheme& s) {
+    const int R = s.R, mn = s.m * s.n;
+    std::vector<int> best(R);
+    for (int r = 0; r < R; ++r) best[r] = r;
+    OrderCost best_c = order_cost(s, best);
+    if (R <= 8) {
+        std::vector<int> p = best;
+        std::sort(p.begin(), p.end());
+        do {
+            OrderCost c = order_cost(s, p);
+            if (c < best_c) { best_c = c; best = p; }
+        } while (std::next_permutation(p.begin(), p.end()));
+    } else {
+        // deterministic restarts (LCG) + first-improvement pairwise-swap descent
+        unsigned long long st = 0x9E3779B97F4A7C15ull;
+        for (int restart = 0; restart < 24; ++restart) {
+            std::vector<int> p(R);
+            for (int r = 0; r < R; ++r) p[r] = r;
+            if (restart > 0)
+                for (int r = R - 1; r > 0; --r) {
+                    st = st * 6364136223846793005ull + 1442695040888963407ull;
+                    std::swap(p[r], p[(int)((st >> 33) % (unsigned long long)(r + 1))]);
+                }
+            OrderCost c = order_cost(s, p);
+            bool improved = true;
+            for (int pass = 0; improved && pass < 8; ++pass) {
+                improved = false;
+                for (int a = 0; a < R; ++a)
+                    for (int b = a + 1; b < R; ++b) {
+                        std::swap(p[a], p[b]);
+                        OrderCost c2 = order_cost(s, p);
+                        if (c2 < c) { c = c2; improved = true; }
+                        else std::swap(p[a], p[b]);
+                    }
+            }
+            if (c < best_c) { best_c = c; best = p; }
+        }
+    }
+    ProductOrder o;
+    o.perm = best;
+    o.max_live = best_c.max_live;
+    // interval colouring: C blocks in order of first use take the lowest slot
+    // whose previous occupant's last use is strictly earlier
+    std::vector<int> first(mn, -1), last(mn, -1);
+    for (int t = 0; t < R; ++t)
+        for (int ij = 0; ij < mn; ++ij)
+            if (s.W[(size_t)best[t] * mn + ij]) {
+                if (first[ij] < 0) first[ij] = t;
+                last[ij] = t;
+            }
+    std::vector<int> idx(mn);
+    for (int ij = 0; ij < mn; ++ij) idx[ij] = ij;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return first[a] < first[b]; });
+    o.slot.assign(mn, 0);
+    std::vector<int> slot_end;   // last use of the current occupant of each slot
+    for (int ij : idx) {
+        int chosen = -1;
+        for (int sl = 0; sl < (int)slot_end.size(); ++sl)
+            if (slot_end[sl] < first[ij]) { chosen = sl; break; }
+        if (chosen < 0) { chosen = (int)slot_end.size(); slot_end.push_back(-1); }
+        slot_end[chosen] = last[ij];
+        o.slot[ij] = chosen;
+    }
+    o.nslot = (int)slot_end.size();
+    return o;
+}
+
+}  // namespace
+
+const ProductOrder& scheme_product_order(int id) {
+    static std::mutex mu;
+    static std::vector<std::unique_ptr<ProductOrder>> cache(256);
+    std::lock_guard<std::mutex> g(mu);
+    if (id < 0 || id >= 256) id = 0;
+    if (!cache[id]) {
+        const Scheme* s = scheme_get(id);
+        cache[id].reset(new ProductOrder(compute_order(*s)));
+    }
+    return *cache[id];
 }
 
 }  // namespace lcma

@@ -36,4 +36,17 @@ int scheme_parse(const std::string& text, Scheme& out, std::string& err);
 long long scheme_brent_failures(const Scheme& s, std::string* first);
 Scheme scheme_compose(const Scheme& outer, const Scheme& inner);
 
+// Processing order of the R products inside a group for the fused Combine H
+// epilogue, chosen to minimise the number of C_ij partial tiles live at the
+// same time (then their total live length), and the resulting assignment of
+// C_ij to shared partial slots (C blocks with disjoint live ranges share one).
+struct ProductOrder {
+    std::vector<int> perm;   // position t -> product r
+    std::vector<int> slot;   // C_ij -> slot
+    int nslot = 0;
+    int max_live = 0;
+};
+// Cached per scheme id; deterministic.
+const ProductOrder& scheme_product_order(int id);
+
 }  // namespace lcma

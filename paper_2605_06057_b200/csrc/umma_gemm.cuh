@@ -47,7 +47,9 @@ struct Cfg {
     static constexpr int kABytes = kBM * 128;                // 128 rows x 128 bytes
     static constexpr int kBBytes = kBNc * 128;               // kBNc x 128 B (K-major) or chunks (MN-major)
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = (196608 / kStageBytes) > 8 ? 8 : (196608 / kStageBytes);
+    // as many stages as fit in 227 KB (minus alignment slack and barriers), <= 8
+    static constexpr int kStages = ((232448 - 1024 - 256) / kStageBytes) > 8 ? 8
+                                                                              : ((232448 - 1024 - 256) / kStageBytes);
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -89,6 +91,10 @@ struct GemmParams {
     float* P;              // partial tiles: [2*ctas][m*n][kBN/4][kBM][4] fp32
     int* flags;            // [ctas] split-segment ready flags
     float* H;              // EPI_STORE_H: H [R][Mb][Nb] fp32
+    int discard;           // 1: discard.global.L2 partial lines after their last read
+    int nslot;             // partial tiles live at once for whole groups (<= m*n)
+    int8_t rperm[kMaxR];   // product processing order inside a group (t -> r)
+    int8_t pslot[kMaxMN];  // shared partial slot of C_ij for whole groups
     int8_t Wc[kMaxR * kMaxMN];   // W[r][i*n + j]
 };
 
@@ -238,9 +244,20 @@ __device__ __forceinline__ void store_c8(const GemmParams& p, long long row, lon
 
 // Partial tile layout: [kBN/4][kBM][4] floats, so that the 32 threads of a
 // warp (32 consecutive rows) touch 512 contiguous bytes per float4 access.
+// Whole groups use the shared slot map pslot (C blocks whose live ranges in
+// the product order do not overlap reuse a tile); split segments keep one
+// tile per C block (they stay live until the owner merges them).
 template <int BN = kBN>
-__device__ __forceinline__ float* partial_tile(const GemmParams& p, int slot, int ij) {
-    return p.P + ((size_t)slot * p.m * p.n + ij) * (size_t)(kBM * BN);
+__device__ __forceinline__ float* partial_tile(const GemmParams& p, int slot, int ij, bool whole) {
+    return p.P + ((size_t)slot * p.m * p.n + (whole ? p.pslot[ij] : ij)) * (size_t)(kBM * BN);
+}
+// Drop the 128-byte L2 lines of a partial tile column range after their last
+// read: dead data is neither written back to DRAM nor occupies L2.  Called by
+// lanes whose row is a multiple of 8 (one line = 8 rows x 16 bytes).
+__device__ __forceinline__ void discard_lines(const float* pt, int row, int col4_0, int n_col4) {
+    for (int c = 0; c < n_col4; ++c)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(pt + ((size_t)(col4_0 + c) * kBM + row) * 4)
+                     : "memory");
 }
 __device__ __forceinline__ size_t partial_off(int row, int col4) {
     return ((size_t)col4 * kBM + row) * 4;
@@ -325,7 +342,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             while (it.next(u)) {
                 int x, z;
                 group_xz(p, u.g, x, z);
-                for (int r = u.r0; r < u.r1; ++r) {
+                for (int t = u.r0; t < u.r1; ++t) {
+                    const int r = p.rperm[t];
                     const int a_row = r * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
                     const int b_col0 = z * BN + (int)rank * C_::kBNc;
                     for (int kb = 0; kb < p.nK; ++kb) {
@@ -440,19 +458,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             group_xz(p, u.g, x, z);
             // rows of this CTA inside the block grid
             const long long brow = (long long)x * C_::kTileM + (long long)rank * kBM + row;
-            // first / last contributing r of each C_ij inside this unit
+            // first / last contributing position t (product order rperm) of each
+            // C_ij inside this unit
             int first_r[kMaxMN], last_r[kMaxMN];
             for (int ij = 0; ij < mn; ++ij) {
                 first_r[ij] = -1;
                 last_r[ij] = -1;
-                for (int r = u.r0; r < u.r1; ++r)
-                    if (p.Wc[r * mn + ij]) {
-                        if (first_r[ij] < 0) first_r[ij] = r;
-                        last_r[ij] = r;
+                for (int t = u.r0; t < u.r1; ++t)
+                    if (p.Wc[p.rperm[t] * mn + ij]) {
+                        if (first_r[ij] < 0) first_r[ij] = t;
+                        last_r[ij] = t;
                     }
             }
             const int slot = (u.role == ROLE_CONTRIB) ? (int)gridDim.x + (int)blockIdx.x : (int)blockIdx.x;
-            for (int r = u.r0; r < u.r1; ++r) {
+            const bool whole = u.role == ROLE_WHOLE;
+            for (int t = u.r0; t < u.r1; ++t) {
+                const int r = p.rperm[t];
                 timed_wait(&tfull_bar[acc], acc_phase, (p.stats && ew == 0 && lane == 0) ? &w_tfull : nullptr);
                 ptx::tc_fence_after();
                 const uint32_t t_addr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
@@ -487,26 +508,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int wc = p.Wc[r * mn + ij];
                     if (!wc) continue;
                     const float sw = (float)wc;
-                    float* pt = partial_tile<BN>(p, slot, ij);
-                    const bool first = (r == first_r[ij]);
-                    const bool final_here = (r == last_r[ij]) && (u.role == ROLE_WHOLE);
+                    float* pt = partial_tile<BN>(p, slot, ij, whole);
+                    const bool first = (t == first_r[ij]);
+                    const bool final_here = (t == last_r[ij]) && whole;
                     if (final_here) {
                         // last contribution: C_ij = partial + w*H_r, rounded once
                         const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
                         const long long ccol = (long long)j * p.Nb + (long long)z * BN + col_base;
-                        if (!(brow < p.Mb && ccol < (long long)(j + 1) * p.Nb)) continue;
+                        if (brow < p.Mb && ccol < (long long)(j + 1) * p.Nb) {
 #pragma unroll
-                        for (int e = 0; e < BN / 2; e += 8) {
-                            float v[8];
+                            for (int e = 0; e < BN / 2; e += 8) {
+                                float v[8];
 #pragma unroll
-                            for (int t = 0; t < 8; ++t) v[t] = sw * __uint_as_float(raw[e + t]);
-                            if (!first) {
-                                const float4 o0 = ld_cg_f4(pt + partial_off(row, (col_base + e) >> 2));
-                                const float4 o1 = ld_cg_f4(pt + partial_off(row, (col_base + e + 4) >> 2));
-                                v[0] += o0.x; v[1] += o0.y; v[2] += o0.z; v[3] += o0.w;
-                                v[4] += o1.x; v[5] += o1.y; v[6] += o1.z; v[7] += o1.w;
+                                for (int q8 = 0; q8 < 8; ++q8) v[q8] = sw * __uint_as_float(raw[e + q8]);
+                                if (!first) {
+                                    const float4 o0 = ld_cg_f4(pt + partial_off(row, (col_base + e) >> 2));
+                                    const float4 o1 = ld_cg_f4(pt + partial_off(row, (col_base + e + 4) >> 2));
+                                    v[0] += o0.x; v[1] += o0.y; v[2] += o0.z; v[3] += o0.w;
+                                    v[4] += o1.x; v[5] += o1.y; v[6] += o1.z; v[7] += o1.w;
+                                }
+                                store_c8(p, (long long)i * p.Mb + brow, ccol + e, v);
                             }
-                            store_c8(p, (long long)i * p.Mb + brow, ccol + e, v);
+                        }
+                        if (!first && p.discard) {
+                            __syncwarp();      // the 8 lanes sharing a line have read it
+                            if ((row & 7) == 0) discard_lines(pt, row, col_base >> 2, BN / 8);
                         }
                     } else if (first) {
 #pragma unroll
@@ -559,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) v[e] = 0.f;
                     if (first_r[ij] >= 0) {
-                        const float* pt = partial_tile<BN>(p, blockIdx.x, ij);
+                        const float* pt = partial_tile<BN>(p, blockIdx.x, ij, false);
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
                             float4 o = ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
@@ -567,16 +593,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     for (int vw = w + 1; vw <= last_w; ++vw) {
-                        // does unit vw's segment contribute to C_ij?
+                        // does unit vw's segment (positions [lo, hi)) contribute to C_ij?
                         long long lo = (long long)vw * p.tail_c - Tt_base;
                         long long hi = lo + p.tail_c;
                         if (lo < 0) lo = 0;
                         if (hi > p.R) hi = p.R;
                         bool contributes = false;
-                        for (long long r = lo; r < hi; ++r)
-                            if (p.Wc[r * mn + ij]) { contributes = true; break; }
+                        for (long long t = lo; t < hi; ++t)
+                            if (p.Wc[p.rperm[t] * mn + ij]) { contributes = true; break; }
                         if (!contributes) continue;
-                        const float* pt = partial_tile<BN>(p, (int)gridDim.x + vw * CG + (int)rank, ij);
+                        const float* pt = partial_tile<BN>(p, (int)gridDim.x + vw * CG + (int)rank, ij, false);
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
                             float4 o = ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
