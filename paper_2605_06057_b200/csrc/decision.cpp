@@ -96,6 +96,16 @@ double estimate_time_b200(const Scheme& s, double M, double N, double K, const P
         const double operand = (Kb / BK) * (128.0 * 128.0 + 128.0 * 128.0);   // A + B half per CTA
         const double rho = partial / operand;
         t += t_mma * (1.0 + hw.alpha_partial * rho * rho);
+        // live partial tiles of all CTAs beyond the L2 budget spill to HBM:
+        // every C_ij update then costs an HBM round trip of the fp32 tile
+        const int nslot = scheme_product_order(s.id).nslot;
+        const double footprint = (double)nslot * 128.0 * tileN * 4.0 * 148.0;
+        if (footprint > hw.l2_partial_budget) {
+            const double groups = (Mb / tileM) * (Nb / tileN);
+            const double tile_bytes = tileM * tileN * 4.0;
+            const double bytes = groups * ((double)s.nnzW() + (double)s.m * s.n) * tile_bytes;
+            t += bytes / (hw.beta * elem_bytes);
+        }
     } else {
         t += t_mma + (R * Mb * Nb * 4.0 + M * N * elem_bytes) / (hw.beta * elem_bytes);
     }

@@ -16,6 +16,7 @@ struct Profile {
     // B200-calibrated model only (decide_b200):
     double beta_combine = 0.0;    // combine kernels' element rate (elements/s)
     double alpha_partial = 0.0;   // fused Combine-H mainloop slowdown coefficient
+    double l2_partial_budget = 64.0 * 1024 * 1024;   // L2 bytes the live partial tiles may use
 };
 
 struct StageCost {

@@ -108,6 +108,7 @@ struct Registry {
         s2.name = "strassen2-4x4x4-r49";
         all.push_back(s2);
         all.push_back(make_laderman());
+        for (int i = 0; i < (int)all.size(); ++i) all[i].id = i;
     }
 };
 
@@ -221,6 +222,7 @@ int scheme_register(const Scheme& s, std::string& err) {
         return -LCMA_ERR_NOT_SUPPORTED;
     }
     R.all.push_back(s);
+    R.all.back().id = (int)R.all.size() - 1;
     return (int)R.all.size() - 1;
 }
 
