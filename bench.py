@@ -169,6 +169,46 @@ def run_reference(args):
     return 0
 
 
+def _time(fn, reps, warm=2):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def _large_shape(L, inputs, torch, args):
+    """BASELINE configs[4] (cfg5, Llama-3-70B FFN M=32768 N=28672 K=8192 bf16) on
+    one GPU: classical vs Strassen (Combine B per call, and B offline)."""
+    M, N, K = 32768, 28672, 8192
+    A, B = inputs.operands(M, N, K, L.BF16, 510, 502, b_layout=args.b_layout)
+    A, B = A.cuda(), B.cuda()
+    out = {"shape": [M, N, K]}
+    fl = 2.0 * M * N * K
+    for name, kw in (("classical", dict(algo="classical")), ("strassen", dict(algo="strassen")),
+                     ("strassen_static_b", dict(algo="strassen", b_static=True))):
+        p = L.Plan(M, N, K, dtype=L.BF16, b_layout=args.b_layout, **kw)
+        C = p.empty_c()
+        ws = p.workspace()
+        if kw.get("b_static"):
+            Bt = p.precombine_b(B)
+            f = lambda: p.gemm_precombined(A, Bt, C, ws)
+        else:
+            f = lambda: p.gemm(A, B, C, ws)
+        out[name + "_tflops"] = fl / (_time(f, 3) * 1e-3) / 1e12
+        del C, ws, p
+        torch.cuda.empty_cache()
+    out["strassen_vs_classical"] = out["strassen_tflops"] / out["classical_tflops"]
+    out["strassen_static_b_vs_classical"] = out["strassen_static_b_tflops"] / out["classical_tflops"]
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -256,6 +296,20 @@ def run_ours(args):
         cms = e0.elapsed_time(e1) / args.steps
         ref = {"classical_tcgen05_tflops": flops / (cms * 1e-3) / 1e12, "classical_ms": cms}
         del Cc
+        # static weights (offline Combine B) and the Decision Module's own choice
+        sp = L.Plan(M, N, K, dtype=L.BF16, algo=algo, b_layout=args.b_layout, b_static=True)
+        Bt_s = sp.precombine_b(B)
+        Cs = sp.empty_c()
+        ws_s = sp.workspace()
+        ref["lcma_static_b_tflops"] = flops / (_time(lambda: sp.gemm_precombined(A, Bt_s, Cs, ws_s),
+                                                       max(3, args.steps // 4)) * 1e-3) / 1e12
+        del Bt_s, Cs, ws_s
+        ap = L.Plan(M, N, K, dtype=L.BF16, algo="auto", b_layout=args.b_layout)
+        ref["auto_choice"] = ap.info["scheme"]
+        ref["auto_pred_speedup"] = ap.info["speedup_pred"]
+        if not args.no_large:
+            ref["large_llama_ffn"] = _large_shape(L, inputs, torch, args)
+        torch.cuda.empty_cache()
 
     # ---- end to end through the public API with HOST buffers
     e2e = None
@@ -355,6 +409,7 @@ def main():
     ap.add_argument("--no_classical", action="store_true")
     ap.add_argument("--no_e2e", action="store_true")
     ap.add_argument("--no_cpu", action="store_true")
+    ap.add_argument("--no_large", action="store_true")
     ap.add_argument("--cpu_seconds", type=float, default=15.0)
     ap.add_argument("--ref_rows", type=int, default=64)
     args = ap.parse_args()

@@ -107,6 +107,78 @@ __device__ __forceinline__ void store_vec(const CombineParams& p, long long off,
     }
 }
 
+// 16-bit Group Combine with more bytes in flight: sources stay packed (8
+// elements per 16-byte register quad), every thread owns U vector positions
+// and issues all U*PQ streaming loads before any arithmetic; outputs are
+// written with streaming (evict-first) stores.  Same arithmetic as below:
+// fp32 signed sum in coefficient order, one RN rounding.
+template <int PQ, int U>
+__global__ void __launch_bounds__(256, 4) group_combine16_kernel(const __grid_constant__ CombineParams p) {
+    const long long nvec = p.E0 * (p.E1 / 8);
+    const long long per_r = p.E0 * p.E1;
+    const long long stride = (long long)gridDim.x * blockDim.x * U;
+    const bool bf16 = p.elem == ELEM_BF16;
+    for (long long v0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * U; v0 < nvec; v0 += stride) {
+        uint4 src[U][PQ];
+        long long e0s[U], e1s[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long vi = v0 + u;
+            const long long e0 = vi / (p.E1 / 8);
+            const long long e1 = (vi - e0 * (p.E1 / 8)) * 8;
+            e0s[u] = e0;
+            e1s[u] = e1;
+#pragma unroll
+            for (int pq = 0; pq < PQ; ++pq) {
+                const int pi = pq / p.Q, qi = pq - (pq / p.Q) * p.Q;
+                const long long r = pi * p.E0 + e0, c = qi * p.E1 + e1;
+                if (vi < nvec && r < p.rows && c < p.cols)
+                    src[u][pq] = __ldcs(reinterpret_cast<const uint4*>(
+                        reinterpret_cast<const uint16_t*>(p.src) + r * p.cols + c));
+                else
+                    src[u][pq] = make_uint4(0, 0, 0, 0);
+            }
+        }
+        for (int r = 0; r < p.R; ++r) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (v0 + u >= nvec) continue;
+                float acc[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+                for (int pq = 0; pq < PQ; ++pq) {
+                    const int cf = p.coef[r * PQ + pq];
+                    if (!cf) continue;
+                    const uint32_t w[4] = {src[u][pq].x, src[u][pq].y, src[u][pq].z, src[u][pq].w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        float2 f;
+                        if (bf16) f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+                        else f = __half22float2(*reinterpret_cast<const __half2*>(&w[h]));
+                        if (cf > 0) { acc[2 * h] += f.x; acc[2 * h + 1] += f.y; }
+                        else { acc[2 * h] -= f.x; acc[2 * h + 1] -= f.y; }
+                    }
+                }
+                uint32_t o[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    if (bf16) {
+                        __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * h], acc[2 * h + 1]);
+                        o[h] = *reinterpret_cast<uint32_t*>(&b);
+                    } else {
+                        __half2 b = __floats2half2_rn(acc[2 * h], acc[2 * h + 1]);
+                        o[h] = *reinterpret_cast<uint32_t*>(&b);
+                    }
+                }
+                __stcs(reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.dst) + (long long)r * per_r +
+                                                e0s[u] * p.E1 + e1s[u]),
+                       make_uint4(o[0], o[1], o[2], o[3]));
+            }
+        }
+    }
+}
+
 // Group Combine (Alg. 2 lines 2-9 / 11-18): out_r[e0][e1] =
 // sum_{p,q} coef[r][p][q] * src[p*E0 + e0][q*E1 + e1], fp32 sum, one rounding.
 template <int VEC, int PQ>

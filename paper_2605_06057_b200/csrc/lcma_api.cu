@@ -580,6 +580,15 @@ lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, boo
                 c.coef[r * inst + a * Q + b] = v;
             }
     const bool fp32 = c.elem == ELEM_FP32;
+    if (!fp32 && (inst == 9 || inst == 16) && !std::getenv("LCMA_OLD_COMBINE")) {
+        // 16-bit sources with 9 or 16 blocks: packed sources keep more loads in
+        // flight (measured 1.4x / 2.3x faster than the unpacked kernel below)
+        const long long nv = c.E0 * (c.E1 / 8);
+        const int g = grid_for(nv, 256);
+        if (inst == 9) group_combine16_kernel<9, 1><<<g, 256, 0, st>>>(c);
+        else group_combine16_kernel<16, 1><<<g, 256, 0, st>>>(c);
+        return check_launch("group_combine16_kernel");
+    }
     const int vec = (fp32 || inst > 9) ? 4 : 8;
     const long long nvec = c.E0 * (c.E1 / vec);
     const int grid = grid_for(nvec, 256);
@@ -701,6 +710,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     }
     g.discard = 1;
     if (const char* dc = std::getenv("LCMA_DISCARD")) g.discard = std::atoi(dc);
+    if (const char* pn = std::getenv("LCMA_PACE_NS")) g.pace_ns = std::atoi(pn);
     if (t_ev_start) cudaEventRecord(t_ev_start, st);
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));
@@ -850,4 +860,31 @@ extern "C" lcma_status lcma_precombine_b(lcma_plan_t p, const void* B, void* Bt,
 extern "C" void lcma_set_kernel_events(void* ev_start, void* ev_end) {
     t_ev_start = reinterpret_cast<cudaEvent_t>(ev_start);
     t_ev_end = reinterpret_cast<cudaEvent_t>(ev_end);
+}
+
+// Diagnostics: co-resident clusters of `cluster_size` CTAs for the tcgen05
+// GEMM kernel configuration (cudaOccupancyMaxActiveClusters); -1 on error.
+extern "C" int lcma_debug_max_clusters(int cluster_size) {
+    if (cudaFuncSetAttribute(umma_gemm_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg<2, 256>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return -1; }
+    if (cluster_size > 8)
+        cudaFuncSetAttribute(umma_gemm_kernel<2, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(cluster_size);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster_size;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, umma_gemm_kernel<2, 256>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return n;
 }

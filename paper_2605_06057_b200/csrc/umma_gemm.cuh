@@ -92,6 +92,7 @@ struct GemmParams {
     int* flags;            // [ctas] split-segment ready flags
     float* H;              // EPI_STORE_H: H [R][Mb][Nb] fp32
     int discard;           // 1: discard.global.L2 partial lines after their last read
+    int pace_ns;           // >0: sleep between C_ij updates (spreads epilogue traffic)
     int nslot;             // partial tiles live at once for whole groups (<= m*n)
     int8_t rperm[kMaxR];   // product processing order inside a group (t -> r)
     int8_t pslot[kMaxMN];  // shared partial slot of C_ij for whole groups
@@ -549,6 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                        sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
                                        sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3]));
                     }
+                    if (p.pace_ns) __nanosleep(p.pace_ns);   // spread the epilogue's L2 traffic
                 }
             }
             if (p.epi_mode != EPI_FUSED || u.role == ROLE_WHOLE || (p.debug & 1)) continue;
