@@ -366,6 +366,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // only the leader arms its barrier (with both CTAs' bytes);
                             // the peer's TMA completes bytes on the leader's barrier
                             const uint32_t lbar = ptx::mapa_shared(ptx::smem_u32(&full_bar[stage]), 0);
+                            if (p.debug & 16) {   // diagnostics: MMA on stale smem, no operand traffic
+                                if (leader) ptx::mbar_arrive(&full_bar[stage]);
+                                if (++stage == kStages) { stage = 0; phase ^= 1; }
+                                continue;
+                            }
                             if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kStageBytes * CG);
                             ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
                             if (!p.b_mn_major) {
@@ -384,10 +389,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ================================ MMA issuer (leader CTA)
-        if (leader && ptx::elect_one()) {
-            const int k_steps = 4;                        // BK / UMMA_K (32 bytes per step)
+        // The whole warp walks the schedule so that stage / descriptor
+        // arithmetic stays in uniform registers; one lane issues the MMAs and
+        // the commits (a commit tracks the MMAs of the issuing thread).
+        if (leader) {
             const uint32_t b_lbo = p.BK * 128;            // MN-major: chunk stride
             const uint32_t b_kstep = p.b_mn_major ? (uint32_t)(32 / (p.tf32 ? 4 : 2)) * 128u : 32u;
+            const uint32_t smem0 = ptx::smem_u32(smem);
+            // descriptors of stage 0, k-step 0; the start-address field (addr >> 4,
+            // bits [0,14)) of later stages / k-steps is reached by plain addition
+            const uint64_t a_desc0 = ptx::smem_desc_sw128(smem0, 16, 1024);
+            const uint64_t b_desc0 = p.b_mn_major
+                                         ? ptx::smem_desc(smem0 + C_::kABytes, b_lbo, p.b_sbo, p.b_layout_type)
+                                         : ptx::smem_desc_sw128(smem0 + C_::kABytes, 16, 1024);
+            const uint32_t b_step = b_kstep >> 4;
+            constexpr uint32_t kStageStep = C_::kStageBytes >> 4;
+            const bool tf32 = p.tf32 != 0;
+            const uint32_t idesc = p.idesc;
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -398,41 +416,51 @@ __global__ void __launch_bounds__(kThreads, 1)
             Unit u;
             while (it.next(u)) {
                 for (int r = u.r0; r < u.r1; ++r) {
-                    timed_wait(&tempty_bar[acc], acc_phase ^ 1, p.stats ? &w_tempty : nullptr);
+                    timed_wait(&tempty_bar[acc], acc_phase ^ 1, (p.stats && lane == 0) ? &w_tempty : nullptr);
                     ptx::tc_fence_after();
                     const uint32_t d_tmem = tmem_base + acc * BN;
                     for (int kb = 0; kb < p.nK; ++kb) {
-                        timed_wait(&full_bar[stage], phase, p.stats ? &w_full : nullptr);
+                        timed_wait(&full_bar[stage], phase, (p.stats && lane == 0) ? &w_full : nullptr);
                         ptx::tc_fence_after();
-                        const uint32_t sa = ptx::smem_u32(smem + stage * C_::kStageBytes);
-                        const uint32_t sb = sa + C_::kABytes;
+                        const uint64_t ad = a_desc0 + (uint64_t)(stage * kStageStep);
+                        const uint64_t bd = b_desc0 + (uint64_t)(stage * kStageStep);
+                        if (ptx::elect_one()) {
+                            if (tf32) {
 #pragma unroll
-                        for (int ks = 0; ks < k_steps; ++ks) {
-                            const uint64_t adesc = ptx::smem_desc_sw128(sa + ks * 32, 16, 1024);
-                            const uint64_t bdesc =
-                                p.b_mn_major ? ptx::smem_desc(sb + ks * b_kstep, b_lbo, p.b_sbo, p.b_layout_type)
-                                             : ptx::smem_desc_sw128(sb + ks * 32, 16, 1024);
-                            const uint32_t accum = (kb | ks) ? 1u : 0u;
-                            if constexpr (CG == 1) {
-                                if (p.tf32) ptx::mma_tf32_ss(d_tmem, adesc, bdesc, p.idesc, accum);
-                                else ptx::mma_f16_ss(d_tmem, adesc, bdesc, p.idesc, accum);
+                                for (int ks = 0; ks < 4; ++ks) {
+                                    const uint32_t accum = (kb | ks) ? 1u : 0u;
+                                    if constexpr (CG == 1)
+                                        ptx::mma_tf32_ss(d_tmem, ad + 2 * ks, bd + b_step * ks, idesc, accum);
+                                    else
+                                        ptx::mma_tf32_ss_cg2(d_tmem, ad + 2 * ks, bd + b_step * ks, idesc, accum);
+                                }
                             } else {
-                                if (p.tf32) ptx::mma_tf32_ss_cg2(d_tmem, adesc, bdesc, p.idesc, accum);
-                                else ptx::mma_f16_ss_cg2(d_tmem, adesc, bdesc, p.idesc, accum);
+#pragma unroll
+                                for (int ks = 0; ks < 4; ++ks) {
+                                    const uint32_t accum = (kb | ks) ? 1u : 0u;
+                                    if constexpr (CG == 1)
+                                        ptx::mma_f16_ss(d_tmem, ad + 2 * ks, bd + b_step * ks, idesc, accum);
+                                    else
+                                        ptx::mma_f16_ss_cg2(d_tmem, ad + 2 * ks, bd + b_step * ks, idesc, accum);
+                                }
                             }
+                            // smem slot free (in both CTAs) once these MMAs completed
+                            if constexpr (CG == 1) ptx::mma_commit(&empty_bar[stage]);
+                            else ptx::mma_commit_cg2_mc(&empty_bar[stage], 0x3);
                         }
-                        // smem slot free (in both CTAs) once these MMAs completed
-                        if constexpr (CG == 1) ptx::mma_commit(&empty_bar[stage]);
-                        else ptx::mma_commit_cg2_mc(&empty_bar[stage], 0x3);
+                        __syncwarp();
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
                     // accumulator ready (in both CTAs)
-                    if constexpr (CG == 1) ptx::mma_commit(&tfull_bar[acc]);
-                    else ptx::mma_commit_cg2_mc(&tfull_bar[acc], 0x3);
+                    if (ptx::elect_one()) {
+                        if constexpr (CG == 1) ptx::mma_commit(&tfull_bar[acc]);
+                        else ptx::mma_commit_cg2_mc(&tfull_bar[acc], 0x3);
+                    }
+                    __syncwarp();
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
             }
-            if (p.stats) {
+            if (p.stats && lane == 0) {
                 p.stats[blockIdx.x * 8 + 1] = w_tempty;
                 p.stats[blockIdx.x * 8 + 2] = w_full;
                 p.stats[blockIdx.x * 8 + 3] = (unsigned long long)(clock64() - t_start);
@@ -475,17 +503,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool whole = u.role == ROLE_WHOLE;
             for (int t = u.r0; t < u.r1; ++t) {
                 const int r = p.rperm[t];
-                timed_wait(&tfull_bar[acc], acc_phase, (p.stats && ew == 0 && lane == 0) ? &w_tfull : nullptr);
+                if (p.debug & 8) ptx::mbar_wait_sleep(&tfull_bar[acc], acc_phase, 256);
+                else timed_wait(&tfull_bar[acc], acc_phase, (p.stats && ew == 0 && lane == 0) ? &w_tfull : nullptr);
                 ptx::tc_fence_after();
                 const uint32_t t_addr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
                                         (uint32_t)(acc * BN + half * (BN / 2));
                 // drain this thread's 128 accumulator columns, then release the
                 // accumulator to the MMA warp before any global-memory traffic
                 uint32_t raw[BN / 2];
+                if (!(p.debug & 2)) {
 #pragma unroll
-                for (int ch = 0; ch < (BN / 2) / 32; ++ch)
-                    ptx::tmem_ld_32x32b_x32(t_addr + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(&raw[ch * 32]));
-                ptx::tmem_wait_ld();
+                    for (int ch = 0; ch < (BN / 2) / 32; ++ch)
+                        ptx::tmem_ld_32x32b_x32(t_addr + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(&raw[ch * 32]));
+                    ptx::tmem_wait_ld();
+                }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
