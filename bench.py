@@ -183,14 +183,31 @@ def _time(fn, reps, warm=2):
     return e0.elapsed_time(e1) / reps
 
 
+def _interleaved(fns, reps, rounds=5):
+    """Median ms per call of each fn, timed in alternating rounds (rotating
+    order) so that clock / power-cap drift over the run hits every arm alike."""
+    import statistics
+    names = list(fns)
+    res = {n: [] for n in names}
+    for n in names:
+        fns[n]()
+    for k in range(rounds):
+        for j in range(len(names)):
+            n = names[(j + k) % len(names)]
+            res[n].append(_time(fns[n], reps, warm=1))
+    return {n: statistics.median(v) for n, v in res.items()}
+
+
 def _large_shape(L, inputs, torch, args):
     """BASELINE configs[4] (cfg5, Llama-3-70B FFN M=32768 N=28672 K=8192 bf16) on
-    one GPU: classical vs Strassen (Combine B per call, and B offline)."""
+    one GPU: classical vs Strassen (Combine B per call, and B offline),
+    interleaved timing."""
     M, N, K = 32768, 28672, 8192
     A, B = inputs.operands(M, N, K, L.BF16, 510, 502, b_layout=args.b_layout)
     A, B = A.cuda(), B.cuda()
-    out = {"shape": [M, N, K]}
+    out = {"shape": [M, N, K], "timing": "median of 5 interleaved rounds x 2 calls"}
     fl = 2.0 * M * N * K
+    plans, fns = [], {}
     for name, kw in (("classical", dict(algo="classical")), ("strassen", dict(algo="strassen")),
                      ("strassen_static_b", dict(algo="strassen", b_static=True))):
         p = L.Plan(M, N, K, dtype=L.BF16, b_layout=args.b_layout, **kw)
@@ -198,14 +215,17 @@ def _large_shape(L, inputs, torch, args):
         ws = p.workspace()
         if kw.get("b_static"):
             Bt = p.precombine_b(B)
-            f = lambda: p.gemm_precombined(A, Bt, C, ws)
+            fns[name] = (lambda p=p, Bt=Bt, C=C, ws=ws: p.gemm_precombined(A, Bt, C, ws))
         else:
-            f = lambda: p.gemm(A, B, C, ws)
-        out[name + "_tflops"] = fl / (_time(f, 3) * 1e-3) / 1e12
-        del C, ws, p
-        torch.cuda.empty_cache()
+            fns[name] = (lambda p=p, C=C, ws=ws: p.gemm(A, B, C, ws))
+        plans.append(p)
+    med = _interleaved(fns, 2)
+    for name, ms in med.items():
+        out[name + "_tflops"] = fl / (ms * 1e-3) / 1e12
     out["strassen_vs_classical"] = out["strassen_tflops"] / out["classical_tflops"]
     out["strassen_static_b_vs_classical"] = out["strassen_static_b_tflops"] / out["classical_tflops"]
+    del fns, plans
+    torch.cuda.empty_cache()
     return out
 
 
@@ -282,28 +302,24 @@ def run_ours(args):
     # ---- classical tcgen05 kernel on the same box (the no-LCMA reference)
     ref = {}
     if rank == 0 and not args.no_classical and plan.info["algo"] != L.ALGO["classical"]:
+        # classical, this algorithm per call, and static weights (offline
+        # Combine B), timed in interleaved rounds on the same inputs
         cp = L.Plan(M, N, K, dtype=L.BF16, algo="classical", b_layout=args.b_layout)
         Cc = cp.empty_c()
-        for _ in range(3):
-            cp.gemm(A, B, Cc)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            cp.gemm(A, B, Cc)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        cms = e0.elapsed_time(e1) / args.steps
-        ref = {"classical_tcgen05_tflops": flops / (cms * 1e-3) / 1e12, "classical_ms": cms}
-        del Cc
-        # static weights (offline Combine B) and the Decision Module's own choice
         sp = L.Plan(M, N, K, dtype=L.BF16, algo=algo, b_layout=args.b_layout, b_static=True)
         Bt_s = sp.precombine_b(B)
         Cs = sp.empty_c()
         ws_s = sp.workspace()
-        ref["lcma_static_b_tflops"] = flops / (_time(lambda: sp.gemm_precombined(A, Bt_s, Cs, ws_s),
-                                                       max(3, args.steps // 4)) * 1e-3) / 1e12
-        del Bt_s, Cs, ws_s
+        med = _interleaved({"classical": lambda: cp.gemm(A, B, Cc),
+                            "lcma": step,
+                            "lcma_static_b": lambda: sp.gemm_precombined(A, Bt_s, Cs, ws_s)},
+                           max(3, args.steps // 10))
+        cms = med["classical"]
+        ref = {"classical_tcgen05_tflops": flops / (cms * 1e-3) / 1e12, "classical_ms": cms,
+               "lcma_interleaved_tflops": flops / (med["lcma"] * 1e-3) / 1e12,
+               "lcma_static_b_tflops": flops / (med["lcma_static_b"] * 1e-3) / 1e12,
+               "comparison_timing": "median of 5 interleaved rounds (classical / lcma / lcma_static_b)"}
+        del Cc, Bt_s, Cs, ws_s
         ap = L.Plan(M, N, K, dtype=L.BF16, algo="auto", b_layout=args.b_layout)
         ref["auto_choice"] = ap.info["scheme"]
         ref["auto_pred_speedup"] = ap.info["speedup_pred"]
@@ -387,7 +403,8 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
-            "effective_vs_classical": (value / world) / ref["classical_tcgen05_tflops"] if ref else None,
+            "effective_vs_classical": (ref["lcma_interleaved_tflops"] / ref["classical_tcgen05_tflops"]
+                                       if ref else None),
         }
         line.update(ref)
         print(json.dumps(line), flush=True)
@@ -405,7 +422,7 @@ def main():
     ap.add_argument("--algo", default="strassen")
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--static_b", type=int, default=0)
-    ap.add_argument("--b_layout", type=int, default=0)
+    ap.add_argument("--b_layout", type=int, default=1)   # 1: B stored N x K (nn.Linear weight)
     ap.add_argument("--no_classical", action="store_true")
     ap.add_argument("--no_e2e", action="store_true")
     ap.add_argument("--no_cpu", action="store_true")

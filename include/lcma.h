@@ -97,7 +97,8 @@ typedef struct {
     int32_t b_static;         /* 1: lcma_gemm_precombined will be used     */
     int32_t variant;          /* lcma_variant                                      */
     int32_t schedule;         /* 0 auto, 1 lockstep rounds + split tail (cache-aware),
-                                 2 paper's contiguous split-group order           */
+                                 2 paper's contiguous split-group order,
+                                 3 whole groups only (group-parallel, no split)   */
     int32_t num_ctas;         /* 0 = one per SM                                    */
     const lcma_hw_profile* hw;/* NULL -> built-in B200 profile                     */
     int32_t decision_model;   /* algo AUTO: 0 = this build's B200-calibrated model

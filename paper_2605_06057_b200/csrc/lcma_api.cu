@@ -105,8 +105,8 @@ std::vector<HostUnit> host_units(const lcma_plan_s* p, int w) {
     std::vector<HostUnit> out;
     const int R = p->sch.R;
     const int W = p->ctas / p->cg;
-    for (int i = 0; i < p->q; ++i) out.push_back({i * W + w, 0, R, ROLE_WHOLE});
-    const long long Tt = (long long)(p->G - p->q * W) * R;
+    for (int i = 0; i < p->q && i * W + w < p->G; ++i) out.push_back({i * W + w, 0, R, ROLE_WHOLE});
+    const long long Tt = std::max<long long>(0, (long long)(p->G - (long long)p->q * W) * R);
     long long t = std::min<long long>((long long)w * p->tail_c, Tt);
     long long t_end = std::min<long long>(t + p->tail_c, Tt);
     while (t < t_end) {
@@ -126,10 +126,12 @@ void make_schedule(lcma_plan_s* p, int mode) {
     const int W = p->ctas / p->cg;
     if (mode == 2) {
         p->q = 0;                              // paper: contiguous split-group chunks
+    } else if (mode == 3) {
+        p->q = (int)cdiv(p->G, W);             // group-parallel only: whole groups, no split
     } else {
         p->q = p->G / W;                       // lockstep rounds (cache-aware)
     }
-    const long long Tt = (long long)(p->G - p->q * W) * R;
+    const long long Tt = std::max<long long>(0, (long long)(p->G - (long long)p->q * W) * R);
     p->tail_c = Tt > 0 ? (int)cdiv(Tt, W) : 1;
     p->swz = 16;
     p->info.groups = p->G;
@@ -281,7 +283,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             return fail(LCMA_ERR_NOT_SUPPORTED, "problem too large for 32-bit tile coordinates");
         }
         p->G = p->nX * p->nZ;
-        make_schedule(p, d.schedule == 2 ? 2 : 1);
+        make_schedule(p, (d.schedule == 2 || d.schedule == 3) ? d.schedule : 1);
     }
 
     // ---- workspace layout
@@ -694,8 +696,17 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     if (std::getenv("LCMA_STATS")) g.stats = lcma_debug_stats_buffer();
     const int mn = S.m * S.n;
     if (S.R > kMaxR || mn > kMaxMN) return fail(LCMA_ERR_NOT_SUPPORTED, "scheme too large for the fused kernel");
-    for (int r = 0; r < S.R; ++r)
-        for (int ij = 0; ij < mn; ++ij) g.Wc[r * mn + ij] = S.W[(size_t)r * mn + ij];
+    for (int r = 0; r < S.R; ++r) {
+        int nu = 0, nv = 0;
+        for (int q = 0; q < S.m * S.k; ++q) nu += S.U[(size_t)r * S.m * S.k + q] != 0;
+        for (int q = 0; q < S.k * S.n; ++q) nv += S.V[(size_t)r * S.k * S.n + q] != 0;
+        g.dbg_extra[r] = (uint8_t)((std::min(nv, 16) - 1) << 4 | (std::min(nu, 16) - 1));
+        g.nzmask[r] = 0;
+        for (int ij = 0; ij < mn; ++ij) {
+            g.Wc[r * mn + ij] = S.W[(size_t)r * mn + ij];
+            if (S.W[(size_t)r * mn + ij]) g.nzmask[r] |= 1u << ij;
+        }
+    }
     // product order inside a group + shared partial slots (fused Combine H)
     const bool use_order = !std::getenv("LCMA_ORDER") || std::atoi(std::getenv("LCMA_ORDER")) != 0;
     if (use_order && !classical) {

@@ -97,6 +97,8 @@ struct GemmParams {
     int8_t rperm[kMaxR];   // product processing order inside a group (t -> r)
     int8_t pslot[kMaxMN];  // shared partial slot of C_ij for whole groups
     int8_t Wc[kMaxR * kMaxMN];   // W[r][i*n + j]
+    uint32_t nzmask[kMaxR];      // bit ij set iff W[r][ij] != 0
+    uint8_t dbg_extra[kMaxR];    // diagnostics: (nnz(V_r)-1) << 4 | (nnz(U_r)-1)
 };
 
 // ------------------------------------------------------------ scheduling
@@ -114,6 +116,7 @@ struct UnitIter {
     long long t, t_end;  // tail tile cursor
     __device__ UnitIter(const GemmParams& p_, int w_) : p(p_), w(w_), idx(0) {
         long long Tt = (long long)(p.G - p.q * p.W) * p.R;
+        if (Tt < 0) Tt = 0;
         t = (long long)w * p.tail_c;
         t_end = t + p.tail_c;
         if (t_end > Tt) t_end = Tt;
@@ -122,6 +125,7 @@ struct UnitIter {
     __device__ bool next(Unit& u) {
         if (idx < p.q) {
             u.g = idx * p.W + w;
+            if (u.g >= p.G) return false;      // schedule 3: last round of whole groups
             u.r0 = 0;
             u.r1 = p.R;
             u.role = ROLE_WHOLE;
@@ -371,7 +375,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 if (++stage == kStages) { stage = 0; phase ^= 1; }
                                 continue;
                             }
-                            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kStageBytes * CG);
+                            // diagnostics (debug bit 5): extra operand tile loads per product,
+                            // the L2 traffic of Combine A/B done in the producer (nnz(U_r)
+                            // resp. nnz(V_r) source tiles instead of one combined tile)
+                            const int ea = (p.debug & 32) ? (p.dbg_extra[r] & 15) : 0;
+                            const int eb = (p.debug & 32) ? (p.dbg_extra[r] >> 4) : 0;
+                            if (leader)
+                                ptx::mbar_arrive_expect_tx(&full_bar[stage],
+                                                           (C_::kStageBytes + ea * C_::kABytes + eb * C_::kBBytes) * CG);
+                            for (int e = 1; e <= ea; ++e)
+                                ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol,
+                                                     ((r + e) % p.R) * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM,
+                                                     ohint, opol);
+                            for (int e = 1; e <= eb && !p.b_mn_major; ++e)
+                                ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol,
+                                                     ((r + e) % p.R) * p.b_rows_per_r + b_col0, ohint, opol);
                             ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
                             if (!p.b_mn_major) {
                                 ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol);
@@ -487,22 +505,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             group_xz(p, u.g, x, z);
             // rows of this CTA inside the block grid
             const long long brow = (long long)x * C_::kTileM + (long long)rank * kBM + row;
-            // first / last contributing position t (product order rperm) of each
-            // C_ij inside this unit
-            int first_r[kMaxMN], last_r[kMaxMN];
-            for (int ij = 0; ij < mn; ++ij) {
-                first_r[ij] = -1;
-                last_r[ij] = -1;
-                for (int t = u.r0; t < u.r1; ++t)
-                    if (p.Wc[p.rperm[t] * mn + ij]) {
-                        if (first_r[ij] < 0) first_r[ij] = t;
-                        last_r[ij] = t;
-                    }
-            }
+            // C_ij already touched inside this unit (bit ij): first contribution test
+            uint32_t seen = 0;
             const int slot = (u.role == ROLE_CONTRIB) ? (int)gridDim.x + (int)blockIdx.x : (int)blockIdx.x;
             const bool whole = u.role == ROLE_WHOLE;
             for (int t = u.r0; t < u.r1; ++t) {
                 const int r = p.rperm[t];
+                // C_ij that later products of this unit still update
+                uint32_t later = 0;
+                for (int t2 = t + 1; t2 < u.r1; ++t2) later |= p.nzmask[p.rperm[t2]];
                 if (p.debug & 8) ptx::mbar_wait_sleep(&tfull_bar[acc], acc_phase, 256);
                 else timed_wait(&tfull_bar[acc], acc_phase, (p.stats && ew == 0 && lane == 0) ? &w_tfull : nullptr);
                 ptx::tc_fence_after();
@@ -536,31 +547,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                     continue;
                 }
                 // Combine H (Eq. 6): C_ij += W[r,i,j] * H_r for every nonzero W
+                const uint32_t nz = p.nzmask[r];
                 for (int ij = 0; ij < mn; ++ij) {
-                    const int wc = p.Wc[r * mn + ij];
-                    if (!wc) continue;
-                    const float sw = (float)wc;
+                    if (!((nz >> ij) & 1u)) continue;
+                    const float sw = (float)p.Wc[r * mn + ij];
                     float* pt = partial_tile<BN>(p, slot, ij, whole);
-                    const bool first = (t == first_r[ij]);
-                    const bool final_here = (t == last_r[ij]) && whole;
+                    const bool first = !((seen >> ij) & 1u);
+                    const bool final_here = whole && !((later >> ij) & 1u);
                     if (final_here) {
-                        // last contribution: C_ij = partial + w*H_r, rounded once
+                        // last contribution: C_ij = partial + w*H_r, rounded once.
+                        // 32 columns per step: the 8 partial loads are issued
+                        // together (one L2 round trip per step, not per vector)
                         const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
-                        const long long ccol = (long long)j * p.Nb + (long long)z * BN + col_base;
-                        if (brow < p.Mb && ccol < (long long)(j + 1) * p.Nb) {
+                        const long long ccol0 = (long long)j * p.Nb + (long long)z * BN + col_base;
+                        const bool in_range = brow < p.Mb && ccol0 < (long long)(j + 1) * p.Nb;
 #pragma unroll
-                            for (int e = 0; e < BN / 2; e += 8) {
-                                float v[8];
+                        for (int ch = 0; ch < (BN / 2) / 32; ++ch) {
+                            float v[32];
 #pragma unroll
-                                for (int q8 = 0; q8 < 8; ++q8) v[q8] = sw * __uint_as_float(raw[e + q8]);
-                                if (!first) {
-                                    const float4 o0 = ld_cg_f4(pt + partial_off(row, (col_base + e) >> 2));
-                                    const float4 o1 = ld_cg_f4(pt + partial_off(row, (col_base + e + 4) >> 2));
-                                    v[0] += o0.x; v[1] += o0.y; v[2] += o0.z; v[3] += o0.w;
-                                    v[4] += o1.x; v[5] += o1.y; v[6] += o1.z; v[7] += o1.w;
+                            for (int e = 0; e < 32; ++e) v[e] = sw * __uint_as_float(raw[ch * 32 + e]);
+                            if (!first) {
+                                float4 o[8];
+#pragma unroll
+                                for (int q = 0; q < 8; ++q)
+                                    o[q] = ld_cg_f4(pt + partial_off(row, (col_base + ch * 32 + 4 * q) >> 2));
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) {
+                                    v[4 * q] += o[q].x; v[4 * q + 1] += o[q].y;
+                                    v[4 * q + 2] += o[q].z; v[4 * q + 3] += o[q].w;
                                 }
-                                store_c8(p, (long long)i * p.Mb + brow, ccol + e, v);
                             }
+                            if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol0 + ch * 32, v);
                         }
                         if (!first && p.discard) {
                             __syncwarp();      // the 8 lanes sharing a line have read it
@@ -583,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (p.pace_ns) __nanosleep(p.pace_ns);   // spread the epilogue's L2 traffic
                 }
+                seen |= nz;
             }
             if (p.epi_mode != EPI_FUSED || u.role == ROLE_WHOLE || (p.debug & 1)) continue;
 
@@ -617,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float v[32];
 #pragma unroll
                     for (int e = 0; e < 32; ++e) v[e] = 0.f;
-                    if (first_r[ij] >= 0) {
+                    if ((seen >> ij) & 1u) {
                         const float* pt = partial_tile<BN>(p, blockIdx.x, ij, false);
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {

@@ -146,3 +146,19 @@ def test_schedule_lockstep_mode_properties():
         for t in range(q * R):
             assert len({a[t][1] for a in per}) == 1
         assert O.r_alignment(per) >= O.r_alignment(O.plan_split_group(G, R, W).assignments)
+
+
+def test_schedule_group_parallel_only_mode():
+    # schedule=3: whole groups round-robin, no split (the ablation step before
+    # Split-Group): complete, never split, ceil(G/W)*R waves
+    for (M, N, K, algo, ctas) in [(8192, 14336, 4096, "strassen", 0), (1536, 2304, 512, "strassen", 6),
+                                  (2048, 3072, 512, "laderman", 10)]:
+        plan = L.Plan(M, N, K, algo=algo, num_ctas=ctas, schedule=3)
+        per = _flatten(plan)
+        G, R = plan.info["groups"], plan.info["R"]
+        assert sorted(x for a in per for x in a) == [(g, r) for g in range(G) for r in range(R)]
+        assert plan.info["split_groups"] == 0
+        W = len(per)
+        assert plan.info["waves"] == -(-G // W) * R
+        for w, a in enumerate(per):
+            assert [g for g, _ in a[::R]] == list(range(w, G, W))

@@ -49,6 +49,12 @@ def main():
                     ws = p.workspace()
                     t[algo] = timeit(lambda: p.gemm(A, B, C, ws))
                     del ws, C, p
+                # Combine B offline (static weights): for model fitting only
+                ps = L.Plan(M, N, K, dtype=dtype, algo="strassen", b_static=True)
+                Cs, wss = ps.empty_c(), ps.workspace()
+                Bts = ps.precombine_b(B)
+                t_sb = timeit(lambda: ps.gemm_precombined(A, Bts, Cs, wss))
+                del ps, Cs, wss, Bts
                 auto = L.Plan(M, N, K, dtype=dtype, algo="auto")
                 paper = L.Plan(M, N, K, dtype=dtype, algo="auto", decision_model=1)
                 best = min(t, key=t.get)
@@ -58,7 +64,8 @@ def main():
                        "eff_tflops": {k: round(2 * M * N * K / v / 1e9, 1) for k, v in t.items()},
                        "best": best, "auto_b200": ch, "auto_paper": chp,
                        "regret_b200": round(t[ch] / t[best], 4), "regret_paper": round(t[chp] / t[best], 4),
-                       "pred_speedup_b200": round(auto.info["speedup_pred"], 4)}
+                       "pred_speedup_b200": round(auto.info["speedup_pred"], 4),
+                       "strassen_static_b_ms": round(t_sb, 4)}
                 rows.append(row)
                 print(json.dumps(row), flush=True)
                 del A, B
@@ -76,7 +83,9 @@ def main():
     }
     print(json.dumps(summ), flush=True)
     os.makedirs("profiles", exist_ok=True)
-    with open("gpurun_out/r01_cfg3_decision.json" if os.path.isdir("gpurun_out") else "r01_cfg3_decision.json", "w") as f:
+    out = os.environ.get("CFG3_OUT", "gpurun_out/r01_cfg3_decision.json")
+    os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
+    with open(out, "w") as f:
         json.dump({"summary": summ, "rows": rows}, f, indent=1)
 
 

@@ -18,15 +18,16 @@ def t(fn, reps=10):
 
 
 M, N, K = [int(v) for v in (sys.argv[1:4] if len(sys.argv) > 3 else (8192, 14336, 4096))]
-A, B = inputs.operands(M, N, K, 0, 1, 2, b_layout=1)
+BL = int(os.environ.get("BL", "1"))
+A, B = inputs.operands(M, N, K, 0, 1, 2, b_layout=BL)
 A, B = A.cuda(), B.cuda()
 for algo in ("classical", "strassen"):
-    p = L.Plan(M, N, K, dtype=0, algo=algo, b_layout=1, b_static=(algo != "classical"))
+    p = L.Plan(M, N, K, dtype=0, algo=algo, b_layout=BL, b_static=(algo != "classical"))
     C = p.empty_c(); ws = p.workspace()
     Bt = p.precombine_b(B) if algo != "classical" else None
     for dbg in sys.argv[4:] or ("0", "4", "1", "5"):
         os.environ["LCMA_DEBUG"] = dbg
         f = (lambda: p.gemm(A, B, C, ws)) if Bt is None else (lambda: p.gemm_precombined(A, Bt, C, ws))
         us = t(f)
-        print(f"{M}x{N}x{K} {algo:10s} debug={dbg} {us:8.1f} us {2*M*N*K/us/1e6:7.1f} TF", flush=True)
+        print(f"{M}x{N}x{K} bl={BL} {algo:10s} debug={dbg} {us:8.1f} us {2*M*N*K/us/1e6:7.1f} TF", flush=True)
     os.environ["LCMA_DEBUG"] = "0"
