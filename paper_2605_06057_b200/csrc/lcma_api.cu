@@ -293,7 +293,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     if (!classical) {
         if (d.dtype != LCMA_FP32 && variant == LCMA_VARIANT_FUSED_H) {
             p->off_P = off;
-            off = align256(off + (size_t)2 * p->ctas * mn * kBM * p->bn * sizeof(float));
+            off = align256(off + (size_t)3 * p->ctas * mn * kBM * p->bn * sizeof(float));
             p->off_flags = off;
             off = align256(off + (size_t)p->ctas * sizeof(int));
         }
@@ -690,6 +690,9 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     g.M = p->d.M; g.N = p->d.N; g.Mb = p->Mb; g.Nb = p->Nb; g.ldc = p->d.N;
     g.C = C; g.P = P; g.flags = flags; g.H = H;
     if (const char* dbg = std::getenv("LCMA_DEBUG")) g.debug = std::atoi(dbg);
+    // fused Combine H partials carry an L2 evict_last policy (measured: -1 %
+    // at cfg2, -3..7 % at the cfg5 shard; profiles/r01b_l2_residency.txt)
+    g.partial_hint = 1;
     if (const char* ph = std::getenv("LCMA_PARTIAL_HINT")) g.partial_hint = std::atoi(ph);
     if (const char* oh = std::getenv("LCMA_OPERAND_HINT")) g.operand_hint = std::atoi(oh);
     if (const char* sw = std::getenv("LCMA_SWZ")) g.swz = std::max(1, std::atoi(sw));
@@ -728,13 +731,41 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     cfg.gridDim = dim3(p->ctas);
     cfg.blockDim = dim3(kThreads);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p->cg;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p->cg == 2) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = p->cg;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    // optional: keep the whole-group partial slots L2-resident (access-policy
+    // window over [P, P + nslot*ctas tiles), persisting)
+    if (P && g.epi_mode == EPI_FUSED && std::getenv("LCMA_L2PERSIST")) {
+        size_t want = (size_t)std::atoll(std::getenv("LCMA_L2PERSIST")) << 20;
+        int maxp = 0, dev0 = 0;
+        cudaGetDevice(&dev0);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev0);
+        want = std::min(want, (size_t)maxp);
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        int maxw = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        const size_t region = (size_t)g.nslot * p->ctas * kBM * p->bn * sizeof(float);
+        const size_t nb = std::min(region, (size_t)maxw);
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = P;
+        attr[na].val.accessPolicyWindow.num_bytes = nb;
+        attr[na].val.accessPolicyWindow.hitRatio = nb ? (float)std::min(1.0, (double)want / (double)nb) : 0.f;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = p->cg == 2 ? 1 : 0;
+    cfg.numAttrs = na;
     cudaError_t e;
     if (p->cg == 2 && p->bn == 256) {
         cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;

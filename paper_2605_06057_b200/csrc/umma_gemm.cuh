@@ -88,7 +88,7 @@ struct GemmParams {
     long long Mb, Nb;      // block extents: C_ij origin = (i*Mb, j*Nb)
     long long ldc;
     void* C;
-    float* P;              // partial tiles: [2*ctas][m*n][kBN/4][kBM][4] fp32
+    float* P;              // partial tiles (see partial_tile), each [kBN/4][kBM][4] fp32
     int* flags;            // [ctas] split-segment ready flags
     float* H;              // EPI_STORE_H: H [R][Mb][Nb] fp32
     int discard;           // 1: discard.global.L2 partial lines after their last read
@@ -173,7 +173,11 @@ __device__ __forceinline__ void red_add_f4(float* p, float a, float b, float c, 
     asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
 }
-// Store 8 consecutive fp32 values (cols c0..c0+7) of one C row, cropped.
+__device__ __forceinline__ void red_add_pol_f4(float* p, float a, float b, float c, float d, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d), "l"(pol)
+                 : "memory");
+}
 struct GemmParams;
 // partial-tile accesses with an L2 cache policy (evict_last keeps the
 // group's C_ij partials resident while operand tiles stream through L2)
@@ -252,9 +256,14 @@ __device__ __forceinline__ void store_c8(const GemmParams& p, long long row, lon
 // Whole groups use the shared slot map pslot (C blocks whose live ranges in
 // the product order do not overlap reuse a tile); split segments keep one
 // tile per C block (they stay live until the owner merges them).
+// Layout: whole-group slots first, slot-major ([nslot][ctas] tiles, one
+// contiguous L2-persistable region), then the split-segment tiles
+// ([2*ctas][m*n]).
 template <int BN = kBN>
 __device__ __forceinline__ float* partial_tile(const GemmParams& p, int slot, int ij, bool whole) {
-    return p.P + ((size_t)slot * p.m * p.n + (whole ? p.pslot[ij] : ij)) * (size_t)(kBM * BN);
+    const size_t T = (size_t)(kBM * BN);
+    if (whole) return p.P + ((size_t)p.pslot[ij] * gridDim.x + slot) * T;
+    return p.P + ((size_t)p.m * p.n * gridDim.x + (size_t)slot * p.m * p.n + ij) * T;
 }
 // Drop the 128-byte L2 lines of a partial tile column range after their last
 // read: dead data is neither written back to DRAM nor occupies L2.  Called by
@@ -584,11 +593,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if ((row & 7) == 0) discard_lines(pt, row, col_base >> 2, BN / 8);
                         }
                     } else if (first) {
+                        if (p.partial_hint) {
+#pragma unroll
+                            for (int e = 0; e < BN / 2; e += 4)
+                                st_pol_f4(pt + partial_off(row, (col_base + e) >> 2),
+                                          make_float4(sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
+                                                      sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3])),
+                                          pol);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < BN / 2; e += 4)
+                                st_cg_f4(pt + partial_off(row, (col_base + e) >> 2),
+                                         make_float4(sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
+                                                     sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3])));
+                        }
+                    } else if (p.partial_hint) {
 #pragma unroll
                         for (int e = 0; e < BN / 2; e += 4)
-                            st_cg_f4(pt + partial_off(row, (col_base + e) >> 2),
-                                     make_float4(sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
-                                                 sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3])));
+                            red_add_pol_f4(pt + partial_off(row, (col_base + e) >> 2),
+                                           sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
+                                           sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3]), pol);
                     } else {
                         // middle contribution: fire-and-forget L2 reduction (same
                         // thread, same address => applied in program order)
