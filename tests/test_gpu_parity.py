@@ -183,6 +183,70 @@ def test_cfg2_full_size_sampled():
     assert np.array_equal(Ci[torch.from_numpy(rows).cuda()].double().cpu().numpy(), refi)
 
 
+def _sampled_rows(M, Mb, n=24, seed=0):
+    rng = np.random.default_rng(seed)
+    edges = [0, 127, 128, 255, 256, Mb - 1, Mb, Mb + 1, 2 * Mb - 1, M - 1]
+    return np.unique(np.concatenate([rng.choice(M, n, replace=False), [r for r in edges if 0 <= r < M]]))
+
+
+def _check_rows(C, A, B, b_layout, rows, eps_rel_max, comp_max):
+    """Sampled rows of C against the fp64 oracle (row-restricted naive GEMM)."""
+    Ad = A[torch.from_numpy(rows)].double().numpy()
+    Bd = _b_dense(B, b_layout).double().numpy()
+    ref = O.gemm_rows_f64(Ad, Bd, np.arange(len(rows)))
+    got = C[torch.from_numpy(rows).to(C.device)].double().cpu().numpy()
+    assert O.eps_rel(got, ref) < eps_rel_max
+    absAB = O.gemm_rows_f64(np.abs(Ad), np.abs(Bd), np.arange(len(rows)))
+    assert (np.abs(got - ref) / absAB).max() < comp_max
+
+
+@pytest.mark.parametrize("algo", ["strassen", "classical"])
+def test_cfg2_bench_layout_sampled(algo):
+    # the exact launch configuration bench.py times: cfg2, B stored N x K
+    M, N, K = 8192, 14336, 4096
+    A, B = inputs.operands(M, N, K, 0, 510, 502, b_layout=1)
+    plan = L.Plan(M, N, K, dtype=L.BF16, algo=algo, b_layout=1)
+    C = plan.gemm(A.cuda(), B.cuda())
+    rows = _sampled_rows(M, plan.info["Mb"])
+    _check_rows(C, A, B, 1, rows, 1e-2, 4e-3)
+    Ai, Bi = inputs.operands(M, N, K, 0, 503, 504, dist="int", lo=-1, hi=1, b_layout=1)
+    plan = L.Plan(M, N, K, dtype=L.BF16, algo=algo, out_dtype=L.FP32, b_layout=1)
+    Ci = plan.gemm(Ai.cuda(), Bi.cuda())
+    refi = O.gemm_rows_f64(Ai[torch.from_numpy(rows)].double().numpy(), Bi.t().double().numpy(),
+                           np.arange(len(rows)))
+    assert np.array_equal(Ci[torch.from_numpy(rows).cuda()].double().cpu().numpy(), refi)
+
+
+@pytest.mark.parametrize("algo", ["laderman", "strassen2"])
+def test_cfg4_full_size_sampled(algo):
+    # BASELINE cfg4: Laderman <3,3,3;23> and Strassen^2 <4,4,4;49> at 12288^3 bf16
+    M = N = K = 12288
+    A, B = inputs.operands(M, N, K, 0, 401, 402, b_layout=1)
+    plan = L.Plan(M, N, K, dtype=L.BF16, algo=algo, b_layout=1)
+    C = plan.gemm(A.cuda(), B.cuda())
+    rows = _sampled_rows(M, plan.info["Mb"], n=16)
+    _check_rows(C, A, B, 1, rows, 1e-2, 6e-3)
+    assert O.freivalds(C.double().cpu().numpy(), A.double().numpy(), B.t().double().numpy(), trials=1) < 2e-2
+    Ai, Bi = inputs.operands(M, N, K, 0, 403, 404, dist="int", lo=-1, hi=1, b_layout=1)
+    plan = L.Plan(M, N, K, dtype=L.BF16, algo=algo, out_dtype=L.FP32, b_layout=1)
+    Ci = plan.gemm(Ai.cuda(), Bi.cuda())
+    refi = O.gemm_rows_f64(Ai[torch.from_numpy(rows)].double().numpy(), Bi.t().double().numpy(),
+                           np.arange(len(rows)))
+    assert np.array_equal(Ci[torch.from_numpy(rows).cuda()].double().cpu().numpy(), refi)
+
+
+def test_cfg5_full_shape_static_b_sampled():
+    # BASELINE cfg5 shape on one GPU (the bench's large_llama_ffn line): Strassen
+    # with B precombined offline (P:465), sampled rows vs the fp64 oracle
+    M, N, K = 32768, 28672, 8192
+    A, B = inputs.operands(M, N, K, 0, 510, 502, b_layout=1)
+    plan = L.Plan(M, N, K, dtype=L.BF16, algo="strassen", b_layout=1, b_static=True)
+    Bt = plan.precombine_b(B.cuda())
+    C = plan.gemm_precombined(A.cuda(), Bt)
+    rows = _sampled_rows(M, plan.info["Mb"], n=12)
+    _check_rows(C, A, B, 1, rows, 1e-2, 4e-3)
+
+
 def test_error_paths():
     plan = L.Plan(256, 512, 256, dtype=L.BF16, algo="strassen")
     A = torch.zeros(256 * 256 + 8, dtype=torch.bfloat16, device="cuda")
