@@ -40,17 +40,17 @@ __device__ __forceinline__ void load_vec(const CombineParams& p, long long r, lo
         const float4* s = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.src) + off);
 #pragma unroll
         for (int e = 0; e < VEC; e += 4) {
-            float4 t = __ldg(s + e / 4);
+            float4 t = __ldcs(s + e / 4);
             v[e] = t.x; v[e + 1] = t.y; v[e + 2] = t.z; v[e + 3] = t.w;
         }
     } else {
         const uint16_t* s = reinterpret_cast<const uint16_t*>(p.src) + off;
         uint32_t w[VEC / 2];
         if (VEC == 8) {
-            uint4 t = __ldg(reinterpret_cast<const uint4*>(s));
+            uint4 t = __ldcs(reinterpret_cast<const uint4*>(s));
             w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
         } else {
-            uint2 t = __ldg(reinterpret_cast<const uint2*>(s));
+            uint2 t = __ldcs(reinterpret_cast<const uint2*>(s));
             w[0] = t.x; w[1] = t.y;
         }
 #pragma unroll
@@ -85,7 +85,7 @@ __device__ __forceinline__ void store_vec(const CombineParams& p, long long off,
                 a = round_tf32_rna(a); b = round_tf32_rna(b);
                 c = round_tf32_rna(c); dd = round_tf32_rna(dd);
             }
-            d[e / 4] = make_float4(a, b, c, dd);
+            __stcs(d + e / 4, make_float4(a, b, c, dd));
         }
     } else {
         uint32_t w[VEC / 2];
@@ -101,9 +101,9 @@ __device__ __forceinline__ void store_vec(const CombineParams& p, long long off,
         }
         uint16_t* d = reinterpret_cast<uint16_t*>(p.dst) + off;
         if (VEC == 8)
-            *reinterpret_cast<uint4*>(d) = make_uint4(w[0], w[1], w[2], w[3]);
+            __stcs(reinterpret_cast<uint4*>(d), make_uint4(w[0], w[1], w[2], w[3]));
         else
-            *reinterpret_cast<uint2*>(d) = make_uint2(w[0], w[1]);
+            __stcs(reinterpret_cast<uint2*>(d), make_uint2(w[0], w[1]));
     }
 }
 

@@ -544,7 +544,9 @@ lcma_status ensure_smem_attr() {
 int grid_for(long long work, int per_block) {
     long long b = (work + per_block - 1) / per_block;
     if (b < 1) b = 1;
-    if (b > 148 * 16) b = 148 * 16;
+    static const long long cap = std::getenv("LCMA_COMB_BLOCKS") ? std::atoll(std::getenv("LCMA_COMB_BLOCKS"))
+                                                                 : 148 * 16;
+    if (b > cap) b = cap;
     return (int)b;
 }
 
@@ -582,12 +584,13 @@ lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, boo
                 c.coef[r * inst + a * Q + b] = v;
             }
     const bool fp32 = c.elem == ELEM_FP32;
-    if (!fp32 && (inst == 9 || inst == 16) && !std::getenv("LCMA_OLD_COMBINE")) {
+    if (!fp32 && (inst == 4 || inst == 9 || inst == 16) && !std::getenv("LCMA_OLD_COMBINE")) {
         // 16-bit sources with 9 or 16 blocks: packed sources keep more loads in
         // flight (measured 1.4x / 2.3x faster than the unpacked kernel below)
         const long long nv = c.E0 * (c.E1 / 8);
         const int g = grid_for(nv, 256);
         if (inst == 9) group_combine16_kernel<9, 1><<<g, 256, 0, st>>>(c);
+        else if (inst == 4) group_combine16_kernel<4, 1><<<g, 256, 0, st>>>(c);
         else group_combine16_kernel<16, 1><<<g, 256, 0, st>>>(c);
         return check_launch("group_combine16_kernel");
     }
