@@ -389,9 +389,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // resp. nnz(V_r) source tiles instead of one combined tile)
                             const int ea = (p.debug & 32) ? (p.dbg_extra[r] & 15) : 0;
                             const int eb = (p.debug & 32) ? (p.dbg_extra[r] >> 4) : 0;
+                            // diagnostics (debug bit 6): A tile loaded only on even k-blocks,
+                            // i.e. the L2 operand traffic of an A-multicast cluster of 2 pairs
+                            const bool skip_a = (p.debug & 64) && (kb & 1);
                             if (leader)
                                 ptx::mbar_arrive_expect_tx(&full_bar[stage],
-                                                           (C_::kStageBytes + ea * C_::kABytes + eb * C_::kBBytes) * CG);
+                                                           (C_::kStageBytes - (skip_a ? C_::kABytes : 0) +
+                                                            ea * C_::kABytes + eb * C_::kBBytes) * CG);
                             for (int e = 1; e <= ea; ++e)
                                 ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol,
                                                      ((r + e) % p.R) * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM,
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int e = 1; e <= eb && !p.b_mn_major; ++e)
                                 ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol,
                                                      ((r + e) % p.R) * p.b_rows_per_r + b_col0, ohint, opol);
-                            ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
+                            if (!skip_a) ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
                             if (!p.b_mn_major) {
                                 ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol);
                             } else {
