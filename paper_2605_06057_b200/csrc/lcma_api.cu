@@ -692,6 +692,11 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     g.m = S.m; g.n = S.n;
     g.M = p->d.M; g.N = p->d.N; g.Mb = p->Mb; g.Nb = p->Nb; g.ldc = p->d.N;
     g.C = C; g.P = P; g.flags = flags; g.H = H;
+    {
+        const int ce = g.out_type == OUT_FP32 ? 4 : 2;
+        g.c_v8 = ((reinterpret_cast<uintptr_t>(C) & 31) == 0 && (g.ldc * ce) % 32 == 0) ? 1 : 0;
+        if (std::getenv("LCMA_NO_V8")) g.c_v8 = 0;
+    }
     if (const char* dbg = std::getenv("LCMA_DEBUG")) g.debug = std::atoi(dbg);
     // fused Combine H partials carry an L2 evict_last policy (measured: -1 %
     // at cfg2, -3..7 % at the cfg5 shard; profiles/r01b_l2_residency.txt)

@@ -87,6 +87,7 @@ struct GemmParams {
     long long M, N;        // true C extents (crop)
     long long Mb, Nb;      // block extents: C_ij origin = (i*Mb, j*Nb)
     long long ldc;
+    int c_v8;              // C rows 32-byte aligned: 256-bit stores
     void* C;
     float* P;              // partial tiles (see partial_tile), each [kBN/4][kBM][4] fp32
     int* flags;            // [ctas] split-segment ready flags
@@ -195,11 +196,27 @@ __device__ __forceinline__ void st_pol_f4(float* p, float4 v, uint64_t pol) {
 // Store 32 consecutive fp32 values of one C row segment (cols c0..c0+31),
 // cropping to N.  N is a multiple of 8 (TMA rule) so 8-element vectors are
 // either fully inside or fully outside.
+__device__ __forceinline__ void st_v8(void* dst, const uint32_t* w) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                 "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t pack2(const GemmParams& p, float a, float b);
+
+// Store 32 consecutive fp32 values of one C row segment (cols c0..c0+31),
+// cropping to N.  N is a multiple of 8 (TMA rule) so 8-element vectors are
+// either fully inside or fully outside.  With 32-byte aligned rows (c_v8) a
+// thread writes whole 32-byte sectors (256-bit STG).
 __device__ __forceinline__ void store_c_row(const GemmParams& p, long long row, long long c0,
                                             const float* v) {
     if (row >= p.M) return;
     if (p.out_type == OUT_FP32) {
         float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + c0;
+        if (p.c_v8 && c0 + 32 <= p.N) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 8) st_v8(dst + e, reinterpret_cast<const uint32_t*>(v + e));
+            return;
+        }
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
             if (c0 + e < p.N)
@@ -207,24 +224,29 @@ __device__ __forceinline__ void store_c_row(const GemmParams& p, long long row, 
         }
     } else {
         uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + row * p.ldc + c0;
+        uint32_t w[16];
+#pragma unroll
+        for (int h = 0; h < 16; ++h) w[h] = pack2(p, v[2 * h], v[2 * h + 1]);
+        if (p.c_v8 && c0 + 32 <= p.N) {
+            st_v8(dst, w);
+            st_v8(dst + 16, w + 8);
+            return;
+        }
 #pragma unroll
         for (int e = 0; e < 32; e += 8) {
-            if (c0 + e < p.N) {
-                uint32_t w4[4];
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    if (p.out_type == OUT_BF16) {
-                        __nv_bfloat162 b = __floats2bfloat162_rn(v[e + 2 * h], v[e + 2 * h + 1]);
-                        w4[h] = *reinterpret_cast<uint32_t*>(&b);
-                    } else {
-                        __half2 b = __floats2half2_rn(v[e + 2 * h], v[e + 2 * h + 1]);
-                        w4[h] = *reinterpret_cast<uint32_t*>(&b);
-                    }
-                }
-                *reinterpret_cast<uint4*>(dst + e) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-            }
+            if (c0 + e < p.N)
+                *reinterpret_cast<uint4*>(dst + e) = make_uint4(w[e / 2], w[e / 2 + 1], w[e / 2 + 2], w[e / 2 + 3]);
         }
     }
+}
+
+__device__ __forceinline__ uint32_t pack2(const GemmParams& p, float a, float b) {
+    if (p.out_type == OUT_BF16) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t*>(&t);
+    }
+    __half2 t = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&t);
 }
 
 // Store 8 consecutive fp32 values (cols c0..c0+7) of one C row, cropped.
