@@ -133,7 +133,10 @@ void make_schedule(lcma_plan_s* p, int mode) {
     }
     const long long Tt = std::max<long long>(0, (long long)(p->G - (long long)p->q * W) * R);
     p->tail_c = Tt > 0 ? (int)cdiv(Tt, W) : 1;
-    p->swz = 16;
+    // raster band height (tile rows): LCMA rounds touch R operand panels per
+    // tile, so a lower band keeps the round's A panels L2-resident (measured
+    // cfg2 Strassen -1..2 %, classical best at 16; tools/swz_exp*.sh)
+    p->swz = R > 1 ? 8 : 16;
     p->info.groups = p->G;
     p->info.tiles = (int)std::min<long long>((long long)p->G * R, INT32_MAX);
     p->info.ctas = p->ctas;
