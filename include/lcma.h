@@ -120,6 +120,9 @@ typedef struct {
     int32_t lcma_condition;   /* Eq. lcma_condition holds                  */
     int32_t fused_condition;  /* Eq. fused_condition holds                 */
     size_t workspace_bytes, btilde_bytes;
+    int32_t partial_slots;    /* fused Combine H: live fp32 C_ij partial tiles per
+                                 CTA of a whole group (product order + interval
+                                 colouring); 0 for classical / unfused            */
 } lcma_plan_info;
 
 /* Create a plan for C = A*B of shape (M,N,K).  out: new plan on LCMA_OK. */

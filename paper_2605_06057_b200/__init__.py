@@ -56,7 +56,8 @@ class PlanInfo(ctypes.Structure):
                 ("t_pred_classical", ctypes.c_double), ("t_pred_choice", ctypes.c_double),
                 ("speedup_pred", ctypes.c_double), ("memory_bound", ctypes.c_int32),
                 ("lcma_condition", ctypes.c_int32), ("fused_condition", ctypes.c_int32),
-                ("workspace_bytes", ctypes.c_size_t), ("btilde_bytes", ctypes.c_size_t)]
+                ("workspace_bytes", ctypes.c_size_t), ("btilde_bytes", ctypes.c_size_t),
+                ("partial_slots", ctypes.c_int32)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}

@@ -341,6 +341,11 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     I.fused_condition = !classical && condition_lhs(S, (double)d.M, (double)d.N, (double)d.K, true) > ratio;
     I.workspace_bytes = p->ws_bytes;
     I.btilde_bytes = p->bt_bytes;
+    I.partial_slots = 0;
+    if (!classical && d.dtype != LCMA_FP32 && variant == LCMA_VARIANT_FUSED_H) {
+        const bool use_order = !std::getenv("LCMA_ORDER") || std::atoi(std::getenv("LCMA_ORDER")) != 0;
+        I.partial_slots = use_order ? scheme_product_order(p->scheme_id).nslot : S.m * S.n;
+    }
     *out = p;
     return LCMA_OK;
 }

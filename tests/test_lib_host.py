@@ -162,3 +162,26 @@ def test_schedule_group_parallel_only_mode():
         assert plan.info["waves"] == -(-G // W) * R
         for w, a in enumerate(per):
             assert [g for g, _ in a[::R]] == list(range(w, G, W))
+
+
+def test_partial_slots_product_order():
+    # fused Combine H keeps at most m*n live C_ij partials per CTA; the product
+    # order must reach the brute-force minimum for Strassen (3 of 4 C blocks)
+    import itertools
+    m, k, n, R, U, V, W = L.scheme_get(1)
+    T = [set(np.flatnonzero(W[r].reshape(-1))) for r in range(R)]
+    best = R
+    for perm in itertools.permutations(range(R)):
+        first, last = {}, {}
+        for t, r in enumerate(perm):
+            for c in T[r]:
+                first.setdefault(c, t)
+                last[c] = t
+        best = min(best, max(sum(1 for c in first if first[c] <= t <= last[c]) for t in range(R)))
+    assert best == 3
+    assert L.Plan(8192, 14336, 4096, algo="strassen").info["partial_slots"] == best
+    for algo, mn in (("laderman", 9), ("strassen2", 16)):
+        s = L.Plan(12288, 12288, 12288, algo=algo).info["partial_slots"]
+        assert 1 <= s <= mn
+    assert L.Plan(4096, 4096, 4096, algo="classical").info["partial_slots"] == 0
+    assert L.Plan(4096, 4096, 4096, algo="strassen", variant="unfused").info["partial_slots"] == 0
