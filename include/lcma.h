@@ -73,7 +73,13 @@ typedef enum {
     LCMA_VARIANT_UNFUSED = 1,  /* Algorithm 1: At, Bt, H materialised     */
     LCMA_VARIANT_FUSED_H = 2,  /* Algorithm 2: At/Bt materialised by group-parallel
                                   combines, GEMM + Combine H fused       */
-    LCMA_VARIANT_PRODUCER = 3  /* Combine A/B in the GEMM producer, Combine H fused  */
+    LCMA_VARIANT_PRODUCER = 3, /* Combine A/B in the GEMM producer, Combine H fused:
+                                  not built (LCMA_ERR_NOT_SUPPORTED), DESIGN.md s.7 */
+    LCMA_VARIANT_TWO_LEVEL = 4 /* two-level scheme (Strassen^2 = Strassen o Strassen,
+                                  P:663): combines of the composed scheme, then one
+                                  fused-Combine-H GEMM per outer product writing the
+                                  outer H_q in fp32, then the outer Combine H as an
+                                  HBM pass (Eq. 6 at the outer level)               */
 } lcma_variant;
 
 typedef struct lcma_plan_s* lcma_plan_t;

@@ -18,7 +18,7 @@ _LIB_PATH = os.path.join(_HERE, "liblcma.so")
 
 BF16, FP16, TF32, FP32 = 0, 1, 2, 3
 ALGO = {"auto": 0, "classical": 1, "strassen": 2, "strassen2": 3, "laderman": 4, "scheme": 5}
-VARIANT = {"auto": 0, "unfused": 1, "fused_h": 2, "producer": 3}
+VARIANT = {"auto": 0, "unfused": 1, "fused_h": 2, "producer": 3, "two_level": 4}
 STATUS = {0: "LCMA_OK", 1: "LCMA_ERR_INVALID_VALUE", 2: "LCMA_ERR_NOT_SUPPORTED",
           3: "LCMA_ERR_MISALIGNED", 4: "LCMA_ERR_SCHEME_INVALID", 5: "LCMA_ERR_COEFF_RANGE",
           6: "LCMA_ERR_PARSE", 7: "LCMA_ERR_WORKSPACE", 8: "LCMA_ERR_CUDA"}

@@ -92,7 +92,10 @@ struct lcma_plan_s {
     int nX, nZ, G, nK;
     int ctas, cg, bn, q, tail_c, swz;
     size_t off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
+    size_t off_inner = 0;          // two-level: the inner plan's partial slots + flags
+    lcma_plan_s* inner = nullptr;  // two-level: fused GEMM plan of the base scheme
     lcma_plan_info info;
+    ~lcma_plan_s() { delete inner; }
 };
 
 // ---------------------------------------------------------------- schedule
@@ -166,7 +169,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         return fail(LCMA_ERR_NOT_SUPPORTED, "tf32 output is fp32");
     if (d.b_layout != 0 && d.b_layout != 1) return fail(LCMA_ERR_INVALID_VALUE, "b_layout must be 0 or 1");
     if (d.algo < LCMA_ALGO_AUTO || d.algo > LCMA_ALGO_SCHEME) return fail(LCMA_ERR_INVALID_VALUE, "bad algo");
-    if (d.variant < 0 || d.variant > 3) return fail(LCMA_ERR_INVALID_VALUE, "bad variant");
+    if (d.variant < 0 || d.variant > 4) return fail(LCMA_ERR_INVALID_VALUE, "bad variant");
     const int e = elem_bytes(d.dtype);
     if ((d.K * e) % 16 != 0 || (d.N * e) % 16 != 0)
         return fail(LCMA_ERR_MISALIGNED, "K and N row lengths must be multiples of 16 bytes (TMA)");
@@ -228,10 +231,17 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             return fail(LCMA_ERR_NOT_SUPPORTED, "fp32 (SIMT) LCMA runs the unfused variant only");
         }
     } else {
-        if (variant == LCMA_VARIANT_AUTO) variant = LCMA_VARIANT_FUSED_H;
+        // composed schemes run two-level (measured 1.06-1.34x faster than the
+        // flat 49-product fused kernel: its 11 live partials per CTA spill L2)
+        if (variant == LCMA_VARIANT_AUTO)
+            variant = p->sch.base_id >= 0 ? LCMA_VARIANT_TWO_LEVEL : LCMA_VARIANT_FUSED_H;
         if (variant == LCMA_VARIANT_PRODUCER) {
             delete p;
-            return fail(LCMA_ERR_NOT_SUPPORTED, "producer-fused variant not built yet");
+            return fail(LCMA_ERR_NOT_SUPPORTED, "producer-fused variant not built (DESIGN.md section 7)");
+        }
+        if (variant == LCMA_VARIANT_TWO_LEVEL && p->sch.base_id < 0) {
+            delete p;
+            return fail(LCMA_ERR_NOT_SUPPORTED, "two-level variant needs a composed scheme (Strassen^2)");
         }
     }
     p->variant = variant;
@@ -289,6 +299,33 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         make_schedule(p, (d.schedule == 2 || d.schedule == 3) ? d.schedule : 1);
     }
 
+    // ---- two-level: the inner (base-scheme) fused GEMM over the composed
+    // scheme's block extents; its C is the outer H_q (fp32)
+    if (variant == LCMA_VARIANT_TWO_LEVEL) {
+        const Scheme& B0 = *scheme_get(S.base_id);
+        lcma_plan_desc di = d;
+        di.M = (int64_t)B0.m * p->Mb;
+        di.N = (int64_t)B0.n * p->Nb;
+        di.K = (int64_t)B0.k * p->Kb;
+        di.out_dtype = LCMA_FP32;
+        di.algo = LCMA_ALGO_SCHEME;
+        di.scheme_id = S.base_id;
+        di.variant = LCMA_VARIANT_FUSED_H;
+        di.b_static = 0;
+        lcma_plan_t in = nullptr;
+        lcma_status st_in = lcma_plan_ex(&di, &in);
+        if (st_in != LCMA_OK) {
+            delete p;
+            return st_in;
+        }
+        if (in->Mb != p->Mb || in->Nb != p->Nb || in->Kb != p->Kb) {
+            delete in;
+            delete p;
+            return fail(LCMA_ERR_NOT_SUPPORTED, "two-level: inner block extents differ");
+        }
+        p->inner = in;
+    }
+
     // ---- workspace layout
     size_t off = 0;
     p->off_P = p->off_flags = p->off_At = p->off_Bt = p->off_H = 0;
@@ -307,6 +344,13 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         if (variant == LCMA_VARIANT_UNFUSED) {
             p->off_H = off;
             off = align256(off + (size_t)S.R * p->Mb * p->Nb * sizeof(float));
+        }
+        if (variant == LCMA_VARIANT_TWO_LEVEL) {
+            const Scheme& B0 = *scheme_get(S.base_id);
+            p->off_H = off;    // outer H_q, q < R_base: [R_base][m0*Mb][n0*Nb] fp32
+            off = align256(off + (size_t)B0.R * (B0.m * p->Mb) * (B0.n * p->Nb) * sizeof(float));
+            p->off_inner = off;
+            off = align256(off + p->inner->off_At);   // the inner plan's partials + flags
         }
     }
     p->ws_bytes = off;
@@ -346,6 +390,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         const bool use_order = !std::getenv("LCMA_ORDER") || std::atoi(std::getenv("LCMA_ORDER")) != 0;
         I.partial_slots = use_order ? scheme_product_order(p->scheme_id).nslot : S.m * S.n;
     }
+    if (variant == LCMA_VARIANT_TWO_LEVEL) I.partial_slots = p->inner->info.partial_slots;
     *out = p;
     return LCMA_OK;
 }
@@ -619,12 +664,13 @@ lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, boo
     return check_launch("group_combine_kernel");
 }
 
-lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cudaStream_t st) {
-    const Scheme& S = p->sch;
+// Combine H (Eq. 6) of scheme S over H [R][Mb][Nb] fp32 into C (M x N, crop).
+lcma_status launch_combine_h_ex(const lcma_plan_s* p, const Scheme& S, long long Mb, long long Nb, const float* H,
+                                void* C, cudaStream_t st) {
     CombineHParams c;
     std::memset(&c, 0, sizeof(c));
     c.H = H; c.C = C;
-    c.M = p->d.M; c.N = p->d.N; c.Mb = p->Mb; c.Nb = p->Nb; c.ldc = p->d.N;
+    c.M = p->d.M; c.N = p->d.N; c.Mb = Mb; c.Nb = Nb; c.ldc = p->d.N;
     c.m = S.m; c.n = S.n; c.R = S.R;
     c.out_type = p->d.out_dtype == LCMA_FP32 || p->d.out_dtype == LCMA_TF32 ? 2
                  : p->d.out_dtype == LCMA_BF16 ? 0 : 1;
@@ -643,6 +689,9 @@ lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cuda
         default: group_combine_h_kernel<32><<<grid, 256, 0, st>>>(c); break;
     }
     return check_launch("group_combine_h_kernel");
+}
+lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cudaStream_t st) {
+    return launch_combine_h_ex(p, p->sch, p->Mb, p->Nb, H, C, st);
 }
 
 // tcgen05 GEMM: classical (R == 1 over A, B) or the LCMA GEMM stage over the
@@ -869,6 +918,25 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
         rs = launch_simt(p, (const float*)At, (const float*)Bt, H, st);   // Eq. 5
         if (rs != LCMA_OK) return rs;
         return launch_combine_h(p, H, C, st);                              // Eq. 6
+    }
+    if (p->variant == LCMA_VARIANT_TWO_LEVEL) {
+        // inner level: one fused GEMM per outer product q over the contiguous
+        // slices At[q*R0 .. q*R0+R0-1], Bt[...] (r = q*R0 + r2, reading 3),
+        // writing H_q (fp32); outer level: Combine H of the base scheme
+        const Scheme& B0 = *scheme_get(p->sch.base_id);
+        const lcma_plan_s* in = p->inner;
+        float* H = reinterpret_cast<float*>(w + p->off_H);
+        const size_t a_slice = (size_t)B0.R * p->Mb * p->Kb * p->e;
+        const size_t b_slice = (size_t)B0.R * p->Kb * p->Nb * p->e;
+        const size_t h_slice = (size_t)(B0.m * p->Mb) * (B0.n * p->Nb);
+        float* Pi = reinterpret_cast<float*>(w + p->off_inner + in->off_P);
+        int* Fi = reinterpret_cast<int*>(w + p->off_inner + in->off_flags);
+        for (int q = 0; q < B0.R; ++q) {
+            rs = launch_umma(in, static_cast<const uint8_t*>(At) + q * a_slice,
+                             static_cast<const uint8_t*>(Bt) + q * b_slice, H + q * h_slice, Pi, Fi, nullptr, st);
+            if (rs != LCMA_OK) return rs;
+        }
+        return launch_combine_h_ex(p, B0, B0.m * p->Mb, B0.n * p->Nb, H, C, st);
     }
     if (p->variant == LCMA_VARIANT_UNFUSED) {
         float* H = reinterpret_cast<float*>(w + p->off_H);

@@ -109,6 +109,7 @@ struct Registry {
         all.push_back(s2);
         all.push_back(make_laderman());
         for (int i = 0; i < (int)all.size(); ++i) all[i].id = i;
+        all[2].base_id = 1;   // Strassen^2 = Strassen o Strassen
     }
 };
 

@@ -13,6 +13,7 @@ namespace lcma {
 struct Scheme {
     std::string name;
     int id = -1;                   // registry id (set on registration)
+    int base_id = -1;              // >= 0: this scheme is compose(base, base)
     int m = 1, k = 1, n = 1, R = 1;
     std::vector<int8_t> U, V, W;   // R*m*k, R*k*n, R*m*n
     int8_t u(int r, int i, int l) const { return U[(r * m + i) * k + l]; }

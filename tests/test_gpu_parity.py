@@ -66,6 +66,30 @@ def test_lcma_exact(algo, shape, b_layout, variant):
     _exact_case(*shape, algo, b_layout=b_layout, variant=variant)
 
 
+@pytest.mark.parametrize("b_layout", [0, 1])
+@pytest.mark.parametrize("shape", [(1024, 1024, 512), (700, 1032, 264), (2048, 3072, 1024)])
+def test_two_level_exact(shape, b_layout):
+    # Strassen^2 as Strassen o Strassen: inner fused GEMMs write the outer H_q
+    # in fp32, the outer Combine H runs as an HBM pass (LCMA_VARIANT_TWO_LEVEL)
+    plan = _exact_case(*shape, "strassen2", b_layout=b_layout, variant="two_level")
+    assert plan.info["variant"] == L.VARIANT["two_level"] and plan.info["partial_slots"] == 3
+
+
+def test_two_level_float_and_static_b():
+    for dtype, gate in ((0, 2e-2), (1, 3e-3), (2, 3e-3)):
+        e, er, er_emu, fv = _float_case(1032, 1544, 1032, "strassen2", dtype, variant="two_level")
+        assert e <= gate and fv <= gate
+        assert er <= 3.0 * er_emu + 1e-6, (er, er_emu)
+    M, N, K = 1536, 2048, 1024
+    A, B = inputs.operands(M, N, K, 0, 11, 12, b_layout=1)
+    A, B = A.cuda(), B.cuda()
+    p1 = L.Plan(M, N, K, dtype=L.BF16, algo="strassen2", b_layout=1, variant="two_level")
+    p2 = L.Plan(M, N, K, dtype=L.BF16, algo="strassen2", b_layout=1, variant="two_level", b_static=True)
+    assert torch.equal(p1.gemm(A, B), p2.gemm_precombined(A, p2.precombine_b(B)))
+    with pytest.raises(L.LcmaError, match="NOT_SUPPORTED"):
+        L.Plan(M, N, K, dtype=L.BF16, algo="laderman", variant="two_level")
+
+
 @pytest.mark.parametrize("dtype", [1, 2])
 def test_lcma_exact_fp16_tf32(dtype):
     _exact_case(512, 1024, 384, "strassen", dtype=dtype)
