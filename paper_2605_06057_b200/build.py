@@ -31,7 +31,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-cudart", "static", "-I", os.path.join(HERE, "..", "include"),
            "-Xptxas", "-v" if verbose else "-O3",
-           "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
+           "-o", tmp] + os.environ.get("LCMA_NVCC_FLAGS", "").split() + [os.path.join(CSRC, f) for f in SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

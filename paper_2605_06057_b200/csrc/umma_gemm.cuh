@@ -32,6 +32,9 @@
 
 namespace lcma {
 
+#ifndef LCMA_MAX_STAGES
+#define LCMA_MAX_STAGES 4         // smem ring depth (measured best: 4 > 5 > 6 > 7 > 3)
+#endif
 constexpr int kBM = 128;          // rows per CTA (TMEM lanes)
 constexpr int kBN = 256;          // UMMA N = accumulator columns
 constexpr int kThreads = 384;     // 12 warps
@@ -48,8 +51,9 @@ struct Cfg {
     static constexpr int kBBytes = kBNc * 128;               // kBNc x 128 B (K-major) or chunks (MN-major)
     static constexpr int kStageBytes = kABytes + kBBytes;
     // as many stages as fit in 227 KB (minus alignment slack and barriers), <= 8
-    static constexpr int kStages = ((232448 - 1024 - 256) / kStageBytes) > 8 ? 8
-                                                                              : ((232448 - 1024 - 256) / kStageBytes);
+    static constexpr int kStages = ((232448 - 1024 - 256) / kStageBytes) > LCMA_MAX_STAGES
+                                       ? LCMA_MAX_STAGES
+                                       : ((232448 - 1024 - 256) / kStageBytes);
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
