@@ -753,6 +753,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         const int ce = g.out_type == OUT_FP32 ? 4 : 2;
         g.c_v8 = ((reinterpret_cast<uintptr_t>(C) & 31) == 0 && (g.ldc * ce) % 32 == 0) ? 1 : 0;
         if (std::getenv("LCMA_NO_V8")) g.c_v8 = 0;
+        g.c_cs = std::getenv("LCMA_C_CS") ? std::atoi(std::getenv("LCMA_C_CS")) : 0;
     }
     if (const char* dbg = std::getenv("LCMA_DEBUG")) g.debug = std::atoi(dbg);
     // fused Combine H partials carry an L2 evict_last policy (measured: -1 %

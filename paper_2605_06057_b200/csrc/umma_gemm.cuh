@@ -92,6 +92,7 @@ struct GemmParams {
     long long Mb, Nb;      // block extents: C_ij origin = (i*Mb, j*Nb)
     long long ldc;
     int c_v8;              // C rows 32-byte aligned: 256-bit stores
+    int c_cs;              // streaming (evict-first) C stores
     void* C;
     float* P;              // partial tiles (see partial_tile), each [kBN/4][kBM][4] fp32
     int* flags;            // [ctas] split-segment ready flags
@@ -200,10 +201,15 @@ __device__ __forceinline__ void st_pol_f4(float* p, float4 v, uint64_t pol) {
 // Store 32 consecutive fp32 values of one C row segment (cols c0..c0+31),
 // cropping to N.  N is a multiple of 8 (TMA rule) so 8-element vectors are
 // either fully inside or fully outside.
-__device__ __forceinline__ void st_v8(void* dst, const uint32_t* w) {
-    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]),
-                 "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-                 : "memory");
+__device__ __forceinline__ void st_v8(void* dst, const uint32_t* w, bool cs) {
+    if (cs)   // streaming (evict-first): C is written once and never re-read here
+        asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(w[0]), "r"(w[1]),
+                     "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
+    else
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                     "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
 }
 __device__ __forceinline__ uint32_t pack2(const GemmParams& p, float a, float b);
 
@@ -218,7 +224,7 @@ __device__ __forceinline__ void store_c_row(const GemmParams& p, long long row, 
         float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + c0;
         if (p.c_v8 && c0 + 32 <= p.N) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 8) st_v8(dst + e, reinterpret_cast<const uint32_t*>(v + e));
+            for (int e = 0; e < 32; e += 8) st_v8(dst + e, reinterpret_cast<const uint32_t*>(v + e), p.c_cs);
             return;
         }
 #pragma unroll
@@ -232,8 +238,8 @@ __device__ __forceinline__ void store_c_row(const GemmParams& p, long long row, 
 #pragma unroll
         for (int h = 0; h < 16; ++h) w[h] = pack2(p, v[2 * h], v[2 * h + 1]);
         if (p.c_v8 && c0 + 32 <= p.N) {
-            st_v8(dst, w);
-            st_v8(dst + 16, w + 8);
+            st_v8(dst, w, p.c_cs);
+            st_v8(dst + 16, w + 8, p.c_cs);
             return;
         }
 #pragma unroll
