@@ -471,6 +471,108 @@ def run_ours(args):
     return 0
 
 
+def run_cfg5(args):
+    """BASELINE configs[4] (opt-in, `--workload cfg5`): Llama-3-70B FFN GEMM
+    M=32768 N=28672 K=8192 bf16, block rows of A and C over the ranks (strong
+    scaling), with the NCCL all-gather of C inside the timed region,
+    overlapped band by band with the compute (shard.gemm_allgather_overlapped,
+    SURVEY 8(e)/(f)).  A is generated in 4096-row blocks with seed 510+b so it
+    is identical for every world size; B (N x K) uses seed 502 everywhere."""
+    import torch
+    import torch.distributed as dist
+    import paper_2605_06057_b200 as L
+    from paper_2605_06057_b200 import inputs, shard
+
+    world, rank, local = _dist_init()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+    M, N, K = 32768, 28672, 8192
+    r0, r1 = shard.row_block(M, world, rank)
+    blocks = []
+    for b in range(r0 // 4096, -(-r1 // 4096)):
+        Ab, _ = inputs.operands(4096, 8, K, L.BF16, 510 + b, 502)
+        blocks.append(Ab[max(r0, 4096 * b) - 4096 * b:min(r1, 4096 * (b + 1)) - 4096 * b])
+    A = torch.cat(blocks).cuda()
+    _, B = inputs.operands(8, N, K, L.BF16, 510, 502, b_layout=1)
+    B = B.cuda()
+    ml = r1 - r0
+    bands = shard.band_rows(ml, args.bands if world > 1 else 1)
+    plans = {}
+    for b0, b1 in bands:
+        h = b1 - b0
+        if h not in plans:
+            pl = L.Plan(h, N, K, dtype=L.BF16, algo=args.algo, b_layout=1)
+            plans[h] = (pl, pl.workspace())
+    C_local = torch.empty(ml, N, dtype=torch.bfloat16, device="cuda")
+    C_full = torch.empty(M, N, dtype=torch.bfloat16, device="cuda") if world > 1 else C_local
+    comm = torch.cuda.Stream()
+
+    def band(b0, b1):
+        pl, ws = plans[b1 - b0]
+        pl.gemm(A[b0:b1], B, C_local[b0:b1], ws)
+
+    def step():
+        if world > 1:
+            shard.gemm_allgather_overlapped(band, C_local, C_full, bands, comm_stream=comm)
+        else:
+            band(0, ml)
+
+    def timed(fn, n):
+        for _ in range(max(3, args.warmup)):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / n
+        if world > 1:
+            tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt[0])
+        return t
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    ms = timed(step, args.steps)
+    clocks = sampler.stop() if sampler else None
+    compute_ms = timed(lambda: band(0, ml) if len(bands) == 1 else [band(a, b) for a, b in bands], args.steps)
+    gather = None
+    if world > 1:
+        gms = timed(lambda: dist.all_gather_into_tensor(C_full, C_local), max(3, args.steps // 2))
+        by = (world - 1) / world * M * N * 2
+        gather = {"ms": gms, "bus_GBps": by / (gms * 1e-3) / 1e9, "bytes_received_per_gpu": by}
+    if rank == 0:
+        flops = 2.0 * M * N * K
+        line = {
+            "metric": "effective TFLOP/s (2MNK/t)", "value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": "cfg5: Llama-3-70B FFN GEMM M=32768 N=28672 K=8192 bf16, block rows "
+                                   "over ranks + NCCL all-gather of C (BASELINE.json configs[4])",
+                       "algo": args.algo, "rows_per_rank": ml, "bands": len(bands), "b_layout": "NxK",
+                       "parallelism": f"block-rows x{world}",
+                       "l2": "inputs+output > 126 MB L2 (no flush needed)"},
+            "compute_only_ms": compute_ms,
+            "compute_only_tflops": flops / (compute_ms * 1e-3) / 1e12,
+            "allgather": gather, "clocks": clocks,
+            "gpu_launches": sum(1 for _ in bands) * L.Plan.last_launch_count() * args.steps,
+            "e2e": None,
+            "note": "opt-in workload; the default bench line is cfg2 (weak scaling)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -487,9 +589,13 @@ def main():
     ap.add_argument("--no_large", action="store_true")
     ap.add_argument("--cpu_seconds", type=float, default=15.0)
     ap.add_argument("--ref_rows", type=int, default=64)
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"])
+    ap.add_argument("--bands", type=int, default=4)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "cfg5":
+        return run_cfg5(args)
     return run_ours(args)
 
 
