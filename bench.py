@@ -229,6 +229,32 @@ def _large_shape(L, inputs, torch, args):
     return out
 
 
+def _tf32_corner(L, inputs, torch):
+    """BASELINE cfg3's grid corner M=16384, N=K=14336 in tf32 (fp32 storage):
+    4-byte operands halve the relative cost of the fp32 Combine-H partials, so
+    this is where LCMA is measured ahead on B200 (profiles/r01d_cfg3_decision.txt)."""
+    M, N, K = 16384, 14336, 14336
+    A, B = inputs.operands(M, N, K, L.TF32, 301, 302)
+    A, B = A.cuda(), B.cuda()
+    fns, keep = {}, []
+    for name, kw in (("classical", dict(algo="classical")), ("strassen", dict(algo="strassen")),
+                     ("auto", dict(algo="auto"))):
+        p = L.Plan(M, N, K, dtype=L.TF32, **kw)
+        C, ws = p.empty_c(), p.workspace()
+        fns[name] = (lambda p=p, C=C, ws=ws: p.gemm(A, B, C, ws))
+        keep += [p, C, ws]
+    med = _interleaved(fns, 1)
+    fl = 2.0 * M * N * K
+    out = {"shape": [M, N, K], "dtype": "tf32", "timing": "median of 5 interleaved rounds",
+           "auto_choice": keep[6].info["scheme"]}
+    for n, ms in med.items():
+        out[n + "_tflops"] = fl / (ms * 1e-3) / 1e12
+    out["strassen_vs_classical"] = med["classical"] / med["strassen"]
+    del fns, keep
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -332,6 +358,7 @@ def run_ours(args):
         ref["auto_pred_speedup"] = ap.info["speedup_pred"]
         if not args.no_large:
             ref["large_llama_ffn"] = _large_shape(L, inputs, torch, args)
+            ref["cfg3_tf32_corner"] = _tf32_corner(L, inputs, torch)
         torch.cuda.empty_cache()
 
     # ---- end to end through the public API with HOST buffers: every step
