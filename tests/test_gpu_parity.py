@@ -271,6 +271,58 @@ def test_cfg5_full_shape_static_b_sampled():
     _check_rows(C, A, B, 1, rows, 1e-2, 4e-3)
 
 
+def test_cuda_graph_capture_and_streams():
+    # lcma_gemm only enqueues (no allocation, no host sync): capturable in a
+    # CUDA graph; replay equals eager; concurrent plans on two streams
+    M, N, K = 1536, 2304, 1024
+    A, B = inputs.operands(M, N, K, 0, 81, 82, b_layout=1)
+    A, B = A.cuda(), B.cuda()
+    for algo in ("classical", "strassen", "laderman", "strassen2"):
+        plan = L.Plan(M, N, K, dtype=L.BF16, algo=algo, b_layout=1)
+        ws = plan.workspace()
+        ref = plan.gemm(A, B, workspace=ws).clone()
+        C = plan.empty_c()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            plan.gemm(A, B, C, ws, stream=s)
+        for _ in range(3):
+            C.zero_()
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(C, ref), algo
+    p1 = L.Plan(M, N, K, dtype=L.BF16, algo="strassen", b_layout=1)
+    p2 = L.Plan(M, N, K, dtype=L.BF16, algo="classical", b_layout=1)
+    r1, r2 = p1.gemm(A, B).clone(), p2.gemm(A, B).clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    C1, C2 = p1.empty_c(), p2.empty_c()
+    torch.cuda.synchronize()
+    for _ in range(4):
+        with torch.cuda.stream(s1):
+            p1.gemm(A, B, C1, stream=s1)
+        with torch.cuda.stream(s2):
+            p2.gemm(A, B, C2, stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(C1, r1) and torch.equal(C2, r2)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_shapes_exact(seed):
+    # fuzz: random ragged shapes, algorithms, layouts, variants, schedules,
+    # CTA counts -- bit-exact against the int64 oracle
+    rng = np.random.default_rng(1000 + seed)
+    algo = ["strassen", "laderman", "strassen2", "classical"][seed % 4]
+    M = int(rng.integers(1, 1400)); N = int(rng.integers(1, 180)) * 8; K = int(rng.integers(1, 160)) * 8
+    kw = dict(b_layout=int(rng.integers(0, 2)))
+    if algo != "classical":
+        kw["variant"] = ["fused_h", "unfused"][int(rng.integers(0, 2))]
+        if kw["variant"] == "fused_h":
+            kw["schedule"] = int(rng.choice([0, 2, 3]))
+            kw["num_ctas"] = int(rng.choice([0, 2, 8, 20, 64]))
+    _exact_case(M, N, K, algo, **kw)
+
+
 def test_error_paths():
     plan = L.Plan(256, 512, 256, dtype=L.BF16, algo="strassen")
     A = torch.zeros(256 * 256 + 8, dtype=torch.bfloat16, device="cuda")
