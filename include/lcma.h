@@ -177,8 +177,9 @@ lcma_status lcma_plan_schedule(lcma_plan_t plan, int32_t cta, int32_t* units, in
 
 /* Measurement hook: when non-NULL cudaEvent_t handles are set, each later
  * lcma_gemm* call on this thread records ev_start / ev_end on its stream right
- * before / after the tcgen05 GEMM kernel (the dominant kernel), so callers
- * can time it live with CUDA events.  NULL, NULL disables. */
+ * before / after the tcgen05 GEMM kernel (the dominant kernel; for two-level
+ * plans, around all inner GEMM launches), so callers can time it live with
+ * CUDA events.  NULL, NULL disables. */
 void lcma_set_kernel_events(void* ev_start, void* ev_end);
 /* Diagnostics (LCMA_STATS=1 in the environment): copies n per-CTA wait-cycle
  * counters to host memory; returns 0 on success. */

@@ -932,11 +932,17 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
         const size_t h_slice = (size_t)(B0.m * p->Mb) * (B0.n * p->Nb);
         float* Pi = reinterpret_cast<float*>(w + p->off_inner + in->off_P);
         int* Fi = reinterpret_cast<int*>(w + p->off_inner + in->off_flags);
-        for (int q = 0; q < B0.R; ++q) {
+        // the measurement events bracket all inner GEMMs together
+        cudaEvent_t ev0 = t_ev_start, ev1 = t_ev_end;
+        t_ev_start = t_ev_end = nullptr;
+        if (ev0) cudaEventRecord(ev0, st);
+        for (int q = 0; q < B0.R && rs == LCMA_OK; ++q)
             rs = launch_umma(in, static_cast<const uint8_t*>(At) + q * a_slice,
                              static_cast<const uint8_t*>(Bt) + q * b_slice, H + q * h_slice, Pi, Fi, nullptr, st);
-            if (rs != LCMA_OK) return rs;
-        }
+        if (ev1) cudaEventRecord(ev1, st);
+        t_ev_start = ev0;
+        t_ev_end = ev1;
+        if (rs != LCMA_OK) return rs;
         return launch_combine_h_ex(p, B0, B0.m * p->Mb, B0.n * p->Nb, H, C, st);
     }
     if (p->variant == LCMA_VARIANT_UNFUSED) {
