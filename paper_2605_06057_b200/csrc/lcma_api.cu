@@ -560,6 +560,26 @@ lcma_status make_map(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64_t co
     return LCMA_OK;
 }
 
+// MN-major B (rows x cols row-major, cols % epr == 0) as a 3-D map
+// {epr elements (128 B), row, cols/epr chunks}: one box of {epr, box_r, n_chunks}
+// lands as [chunk][row][128 B], the layout the UMMA MN-major descriptor reads.
+lcma_status make_map_mn3d(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64_t cols, uint64_t rows,
+                          uint32_t epr, uint32_t box_r, uint32_t n_chunks, CUtensorMapSwizzle swz) {
+    auto fn = encode_fn();
+    if (!fn) return fail(LCMA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMapDataType t = dt == LCMA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                            : dt == LCMA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const int e = elem_bytes(dt);
+    cuuint64_t dims[3] = {epr, rows, cols / epr};
+    cuuint64_t strides[2] = {cols * (cuuint64_t)e, (cuuint64_t)epr * e};
+    cuuint32_t box[3] = {epr, box_r, n_chunks};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, t, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? LCMA_OK : LCMA_ERR_NOT_SUPPORTED;
+}
+
 // Diagnostics only (LCMA_STATS set): a process-lifetime device buffer for the
 // per-CTA wait-cycle counters; read back with lcma_debug_stats().
 unsigned long long* g_stats = nullptr;
@@ -712,6 +732,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     rs = make_map(&ta, Aop, dt, a_cols, a_rows, epr, kBM);
     if (rs != LCMA_OK) return rs;
     const bool b_mn = p->d.b_layout == 0;
+    bool b3d = false;
     if (!b_mn) {   // N x K (K-major)
         const uint64_t cols = classical ? p->d.K : p->Kb;
         const uint64_t rows = classical ? p->d.N : (uint64_t)S.R * p->Nb;
@@ -724,7 +745,10 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
             if (const char* v = std::getenv("LCMA_TF32_MN_SWZ")) swz = (CUtensorMapSwizzle)std::atoi(v);
             else swz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
         }
-        rs = make_map(&tb, Bop, dt, cols, rows, epr, p->BK, swz);
+        b3d = cols % (uint64_t)epr == 0 && !std::getenv("LCMA_B2D") &&
+              make_map_mn3d(&tb, Bop, dt, cols, rows, epr, p->BK, (uint32_t)((p->bn / p->cg) / p->BK), swz) ==
+                  LCMA_OK;
+        if (!b3d) rs = make_map(&tb, Bop, dt, cols, rows, epr, p->BK, swz);
     }
     if (rs != LCMA_OK) return rs;
 
@@ -734,6 +758,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     g.a_rows_per_r = classical ? 0 : (int)p->Mb;
     g.b_rows_per_r = classical ? 0 : (int)(b_mn ? p->Kb : p->Nb);
     g.b_mn_major = b_mn;
+    g.b_3d = b3d ? 1 : 0;
     // MN-major 32-bit operands use the 128B_BASE32B layout (4-row swizzle atoms)
     g.b_layout_type = (dt == LCMA_TF32) ? 1 : 2;
     g.b_sbo = (dt == LCMA_TF32) ? 512 : 1024;

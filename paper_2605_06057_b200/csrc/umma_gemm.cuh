@@ -71,6 +71,7 @@ struct GemmParams {
     int a_rows_per_r;      // row offset of At_r in the A tensor map (Mb), 0 for R == 1
     int b_rows_per_r;      // row offset of Bt_r in the B map (Nb if K-major else Kb)
     int b_mn_major;        // B operand MN-major (B stored K x N)
+    int b_3d;              // MN-major B via one 3-D TMA box per stage
     int tf32;              // kind::tf32 (else kind::f16)
     uint32_t idesc;        // instruction descriptor
     // schedule
@@ -402,6 +403,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tma_load_2d(sa, &tmap_a, &full_bar[stage], kcol, a_row);
                             if (!p.b_mn_major) {
                                 ptx::tma_load_2d(sb, &tmap_b, &full_bar[stage], kcol, r * p.b_rows_per_r + b_col0);
+                            } else if (p.b_3d) {
+                                ptx::tma_load_3d(sb, &tmap_b, &full_bar[stage], 0, r * p.b_rows_per_r + kcol,
+                                                 b_col0 / p.BK);
                             } else {
                                 for (int c = 0; c < n_chunks; ++c)
                                     ptx::tma_load_2d(sb + c * b_bytes_chunk, &tmap_b, &full_bar[stage],
@@ -438,6 +442,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (!skip_a) ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
                             if (!p.b_mn_major) {
                                 ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol);
+                            } else if (p.b_3d) {
+                                ptx::tma_load_3d_cg2(sb, &tmap_b, lbar, 0, r * p.b_rows_per_r + kcol,
+                                                     b_col0 / p.BK);
                             } else {
                                 for (int c = 0; c < n_chunks; ++c)
                                     ptx::tma_load_2d_cg2(sb + c * b_bytes_chunk, &tmap_b, lbar,
