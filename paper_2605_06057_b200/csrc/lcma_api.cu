@@ -813,6 +813,17 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         for (int ij = 0; ij < mn; ++ij) g.pslot[ij] = (int8_t)ij;
         g.nslot = mn;
     }
+    // the C_ij with the most contributions keeps its column-half-0 partial in
+    // shared memory (whole groups of the fused epilogue)
+    g.smem_ij = -1;
+    if (!classical && !H && mn > 1 && !(std::getenv("LCMA_SMEM_PARTIAL") && std::atoi(std::getenv("LCMA_SMEM_PARTIAL")) == 0)) {
+        int best = 0;
+        for (int ij = 0; ij < mn; ++ij) {
+            int c = 0;
+            for (int r = 0; r < S.R; ++r) c += S.W[(size_t)r * mn + ij] != 0;
+            if (c > best) { best = c; g.smem_ij = ij; }
+        }
+    }
     g.discard = 1;
     if (const char* dc = std::getenv("LCMA_DISCARD")) g.discard = std::atoi(dc);
     if (const char* pn = std::getenv("LCMA_PACE_NS")) g.pace_ns = std::atoi(pn);

@@ -54,7 +54,10 @@ struct Cfg {
     static constexpr int kStages = ((232448 - 1024 - 256) / kStageBytes) > LCMA_MAX_STAGES
                                        ? LCMA_MAX_STAGES
                                        : ((232448 - 1024 - 256) / kStageBytes);
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    // one C_ij partial of the column half 0 kept in shared memory (fused
+    // Combine H, whole groups): 128 rows x BN/2 fp32
+    static constexpr int kPartialSmem = kBM * (BN / 2) * 4;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kPartialSmem + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 enum EpiMode : int { EPI_FUSED = 0, EPI_STORE_H = 1 };
@@ -101,6 +104,7 @@ struct GemmParams {
     int discard;           // 1: discard.global.L2 partial lines after their last read
     int pace_ns;           // >0: sleep between C_ij updates (spreads epilogue traffic)
     int nslot;             // partial tiles live at once for whole groups (<= m*n)
+    int smem_ij;           // C_ij whose column-half-0 partial lives in shared memory (-1: none)
     int8_t rperm[kMaxR];   // product processing order inside a group (t -> r)
     int8_t pslot[kMaxMN];  // shared partial slot of C_ij for whole groups
     int8_t Wc[kMaxR * kMaxMN];   // W[r][i*n + j]
@@ -332,7 +336,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * C_::kStageBytes);
+    float* psmem = reinterpret_cast<float*>(smem + kStages * C_::kStageBytes);   // [BN/8][kBM][4]
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * C_::kStageBytes + C_::kPartialSmem);
     uint64_t* empty_bar = full_bar + kStages;
     uint64_t* tfull_bar = empty_bar + kStages;   // [2]
     uint64_t* tempty_bar = tfull_bar + 2;        // [2]
@@ -606,7 +611,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float* pt = partial_tile<BN>(p, slot, ij, whole);
                     const bool first = !((seen >> ij) & 1u);
                     const bool final_here = whole && !((later >> ij) & 1u);
-                    if (final_here) {
+                    if (whole && ij == p.smem_ij && half == 0) {
+                        // shared-memory partial: this thread alone owns (row, cols
+                        // 0..BN/2-1) of it, so plain loads/stores in program order
+                        float* sp = psmem;
+                        if (final_here) {
+                            const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
+                            const long long ccol0 = (long long)j * p.Nb + (long long)z * BN;
+                            const bool in_range = brow < p.Mb && ccol0 < (long long)(j + 1) * p.Nb;
+#pragma unroll
+                            for (int ch = 0; ch < (BN / 2) / 32; ++ch) {
+                                float v[32];
+#pragma unroll
+                                for (int e = 0; e < 32; e += 4) {
+                                    float4 o = first ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                     : *reinterpret_cast<const float4*>(sp + partial_off(row, (ch * 32 + e) >> 2));
+                                    v[e] = o.x + sw * __uint_as_float(raw[ch * 32 + e]);
+                                    v[e + 1] = o.y + sw * __uint_as_float(raw[ch * 32 + e + 1]);
+                                    v[e + 2] = o.z + sw * __uint_as_float(raw[ch * 32 + e + 2]);
+                                    v[e + 3] = o.w + sw * __uint_as_float(raw[ch * 32 + e + 3]);
+                                }
+                                if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol0 + ch * 32, v);
+                            }
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < BN / 2; e += 4) {
+                                float4* q = reinterpret_cast<float4*>(sp + partial_off(row, e >> 2));
+                                float4 o = first ? make_float4(0.f, 0.f, 0.f, 0.f) : *q;
+                                o.x += sw * __uint_as_float(raw[e]);
+                                o.y += sw * __uint_as_float(raw[e + 1]);
+                                o.z += sw * __uint_as_float(raw[e + 2]);
+                                o.w += sw * __uint_as_float(raw[e + 3]);
+                                *q = o;
+                            }
+                        }
+                    } else if (final_here) {
                         // last contribution: C_ij = partial + w*H_r, rounded once.
                         // 32 columns per step: the 8 partial loads are issued
                         // together (one L2 round trip per step, not per vector)
