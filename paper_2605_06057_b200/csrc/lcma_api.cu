@@ -602,13 +602,13 @@ lcma_status check_launch(const char* what) {
     return LCMA_OK;
 }
 
-template <int CG, int BN>
+template <int CG, int BN, int QF = 0>
 lcma_status ensure_smem_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   Cfg<CG, BN>::kSmemBytes);
+        err = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Cfg<CG, BN, QF>::kSmemBytes);
     });
     if (err != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
     return LCMA_OK;
@@ -718,11 +718,18 @@ lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cuda
 // materialised At / Bt with the fused Combine H (or H store) epilogue.
 lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, void* C, float* P,
                         int* flags, float* H, cudaStream_t st) {
-    lcma_status rs = p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>() : ensure_smem_attr<2, 256>())
-                                : (p->bn == 128 ? ensure_smem_attr<1, 128>() : ensure_smem_attr<1, 256>());
-    if (rs != LCMA_OK) return rs;
     const Scheme& S = p->sch;
     const bool classical = p->scheme_id == SCHEME_CLASSICAL;
+    // QF: the shared-memory partial home covers both column halves (3 operand
+    // stages; measured slower than 4 stages with column half 1 in L2: cfg2
+    // 910 vs 824 us, so opt-in only)
+    int qf = 0;
+    if (const char* v = std::getenv("LCMA_QFULL"))
+        qf = (!classical && !H && p->cg == 2 && p->bn == 256 && S.m * S.n > 1 && std::atoi(v) != 0) ? 1 : 0;
+    lcma_status rs = p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
+                                                : (qf ? ensure_smem_attr<2, 256, 1>() : ensure_smem_attr<2, 256>()))
+                                : (p->bn == 128 ? ensure_smem_attr<1, 128>() : ensure_smem_attr<1, 256>());
+    if (rs != LCMA_OK) return rs;
     const lcma_dtype dt = p->d.dtype;
     const int epr = 128 / p->e;           // elements per 128-byte row
     CUtensorMap ta, tb;
@@ -801,28 +808,36 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
             if (S.W[(size_t)r * mn + ij]) g.nzmask[r] |= 1u << ij;
         }
     }
-    // product order inside a group + shared partial slots (fused Combine H)
+    // product order inside a group + partial homes (fused Combine H, whole
+    // groups): the two C_ij slots with the most partial updates live on chip
+    // (epilogue registers, shared memory), the others in L2 workspace slots
     const bool use_order = !std::getenv("LCMA_ORDER") || std::atoi(std::getenv("LCMA_ORDER")) != 0;
+    for (int ij = 0; ij < kMaxMN; ++ij) g.home[ij] = 0;
     if (use_order && !classical) {
         const ProductOrder& po = scheme_product_order(p->scheme_id);
         for (int t = 0; t < S.R; ++t) g.rperm[t] = (int8_t)po.perm[t];
-        for (int ij = 0; ij < mn; ++ij) g.pslot[ij] = (int8_t)po.slot[ij];
-        g.nslot = po.nslot;
+        // slot -> home
+        const int ns = po.nslot;
+        std::vector<int> by_use(ns);
+        for (int k = 0; k < ns; ++k) by_use[k] = k;
+        std::stable_sort(by_use.begin(), by_use.end(),
+                         [&](int a, int b) { return po.slot_updates[a] > po.slot_updates[b]; });
+        const bool use_reg = !H && !(std::getenv("LCMA_REG_PARTIAL") && std::atoi(std::getenv("LCMA_REG_PARTIAL")) == 0);
+        const bool use_smem = !H && !(std::getenv("LCMA_SMEM_PARTIAL") && std::atoi(std::getenv("LCMA_SMEM_PARTIAL")) == 0);
+        std::vector<int> slot_home(ns, 0);
+        int nl2 = 0, k0 = 0;
+        if (use_reg && k0 < ns) slot_home[by_use[k0++]] = HOME_REG;
+        if (use_smem && k0 < ns) slot_home[by_use[k0++]] = HOME_SMEM;
+        for (int k = k0; k < ns; ++k) slot_home[by_use[k]] = nl2++;
+        g.qslot = nl2;                    // L2 tile of the shared partial's column half 1 (QF = 0)
+        for (int ij = 0; ij < mn; ++ij) g.home[ij] = (int8_t)(po.slot[ij] >= 0 ? slot_home[po.slot[ij]] : 0);
+        g.nslot = nl2 + (use_smem ? 1 : 0);
     } else {
+        // every C_ij keeps its own L2 slot
         for (int t = 0; t < S.R; ++t) g.rperm[t] = (int8_t)t;
-        for (int ij = 0; ij < mn; ++ij) g.pslot[ij] = (int8_t)ij;
+        for (int ij = 0; ij < mn; ++ij) g.home[ij] = (int8_t)ij;
+        g.qslot = 0;
         g.nslot = mn;
-    }
-    // the C_ij with the most contributions keeps its column-half-0 partial in
-    // shared memory (whole groups of the fused epilogue)
-    g.smem_ij = -1;
-    if (!classical && !H && mn > 1 && !(std::getenv("LCMA_SMEM_PARTIAL") && std::atoi(std::getenv("LCMA_SMEM_PARTIAL")) == 0)) {
-        int best = 0;
-        for (int ij = 0; ij < mn; ++ij) {
-            int c = 0;
-            for (int r = 0; r < S.R; ++r) c += S.W[(size_t)r * mn + ij] != 0;
-            if (c > best) { best = c; g.smem_ij = ij; }
-        }
     }
     g.discard = 1;
     if (const char* dc = std::getenv("LCMA_DISCARD")) g.discard = std::atoi(dc);
@@ -869,7 +884,10 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     cfg.attrs = attr;
     cfg.numAttrs = na;
     cudaError_t e;
-    if (p->cg == 2 && p->bn == 256) {
+    if (p->cg == 2 && p->bn == 256 && qf) {
+        cfg.dynamicSmemBytes = Cfg<2, 256, 1>::kSmemBytes;
+        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 1>, ta, tb, g);
+    } else if (p->cg == 2 && p->bn == 256) {
         cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256>, ta, tb, g);
     } else if (p->cg == 2) {

@@ -30,6 +30,18 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
+// Per-warpgroup register reallocation (all four warps of a warpgroup execute
+// the same instruction): the TMA / MMA warpgroup hands registers to the
+// epilogue warpgroups, which keep one fp32 C_ij partial in registers.
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // ------------------------------------------------------------------ mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)

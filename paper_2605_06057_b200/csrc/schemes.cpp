@@ -307,7 +307,12 @@ struct OrderCost {
     }
 };
 
-// Live range of C_ij = [first position contributing, last position contributing].
+// Live range of C_ij = [first position contributing, last position
+// contributing).  A partial must be stored across the boundary after
+// position t iff first <= t < last: the last contribution is consumed
+// straight into the rounded C store, and a home freed by it can take a first
+// contribution of the same product (the epilogue handles last contributions
+// first, element by element in the same thread).
 OrderCost order_cost(const Scheme& s, const std::vector<int>& perm) {
     const int mn = s.m * s.n, R = s.R;
     std::vector<int> first(mn, -1), last(mn, -1);
@@ -320,7 +325,7 @@ OrderCost order_cost(const Scheme& s, const std::vector<int>& perm) {
     OrderCost c{0, 0};
     for (int t = 0; t < R; ++t) {
         int live = 0;
-        for (int ij = 0; ij < mn; ++ij) live += (first[ij] >= 0 && first[ij] <= t && t <= last[ij]);
+        for (int ij = 0; ij < mn; ++ij) live += (first[ij] >= 0 && first[ij] <= t && t < last[ij]);
         c.max_live = std::max(c.max_live, live);
         c.total_live += live;
     }
@@ -369,25 +374,33 @@ ProductOrder compute_order(const Scheme& s) {
     o.perm = best;
     o.max_live = best_c.max_live;
     // interval colouring: C blocks in order of first use take the lowest slot
-    // whose previous occupant's last use is strictly earlier
-    std::vector<int> first(mn, -1), last(mn, -1);
+    // whose previous occupant's last use is not later than this first use
+    std::vector<int> first(mn, -1), last(mn, -1), uses(mn, 0);
     for (int t = 0; t < R; ++t)
         for (int ij = 0; ij < mn; ++ij)
             if (s.W[(size_t)best[t] * mn + ij]) {
                 if (first[ij] < 0) first[ij] = t;
                 last[ij] = t;
+                ++uses[ij];
             }
     std::vector<int> idx(mn);
     for (int ij = 0; ij < mn; ++ij) idx[ij] = ij;
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return first[a] < first[b]; });
-    o.slot.assign(mn, 0);
+    o.slot.assign(mn, -1);
     std::vector<int> slot_end;   // last use of the current occupant of each slot
     for (int ij : idx) {
+        if (first[ij] < 0) continue;
+        if (first[ij] == last[ij]) { o.slot[ij] = -1; continue; }   // single contribution: no partial
         int chosen = -1;
         for (int sl = 0; sl < (int)slot_end.size(); ++sl)
-            if (slot_end[sl] < first[ij]) { chosen = sl; break; }
-        if (chosen < 0) { chosen = (int)slot_end.size(); slot_end.push_back(-1); }
+            if (slot_end[sl] <= first[ij]) { chosen = sl; break; }
+        if (chosen < 0) {
+            chosen = (int)slot_end.size();
+            slot_end.push_back(-1);
+            o.slot_updates.push_back(0);
+        }
         slot_end[chosen] = last[ij];
+        o.slot_updates[chosen] += uses[ij] - 1;   // stored partial accesses (all but the first's store)
         o.slot[ij] = chosen;
     }
     o.nslot = (int)slot_end.size();

@@ -43,9 +43,10 @@ Scheme scheme_compose(const Scheme& outer, const Scheme& inner);
 // same time (then their total live length), and the resulting assignment of
 // C_ij to shared partial slots (C blocks with disjoint live ranges share one).
 struct ProductOrder {
-    std::vector<int> perm;   // position t -> product r
-    std::vector<int> slot;   // C_ij -> slot
-    int nslot = 0;
+    std::vector<int> perm;           // position t -> product r
+    std::vector<int> slot;           // C_ij -> slot (-1: one contribution, never stored)
+    std::vector<int> slot_updates;   // per slot: partial read-modify-writes over a group
+    int nslot = 0;                   // partials live at once (per CTA)
     int max_live = 0;
 };
 // Cached per scheme id; deterministic.

@@ -28,6 +28,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "ptx.cuh"
 
 namespace lcma {
@@ -43,26 +45,33 @@ constexpr int kEpiWarps = 8;
 constexpr int kMaxR = 128;
 constexpr int kMaxMN = 32;
 
-template <int CG, int BN = kBN>
+// QF = 1: the shared-memory C_ij partial covers the whole 128 x BN slab of
+// the CTA (128 KB for BN = 256, leaving room for 3 operand stages); QF = 0:
+// only column half 0 (64 KB, 4 stages), half 1 of that partial goes to L2.
+template <int CG, int BN = kBN, int QF = 0>
 struct Cfg {
     static constexpr int kTileM = kBM * CG;                  // rows per group tile
     static constexpr int kBNc = BN / CG;                     // B columns staged per CTA
     static constexpr int kABytes = kBM * 128;                // 128 rows x 128 bytes
     static constexpr int kBBytes = kBNc * 128;               // kBNc x 128 B (K-major) or chunks (MN-major)
     static constexpr int kStageBytes = kABytes + kBBytes;
-    // as many stages as fit in 227 KB (minus alignment slack and barriers), <= 8
-    static constexpr int kStages = ((232448 - 1024 - 256) / kStageBytes) > LCMA_MAX_STAGES
-                                       ? LCMA_MAX_STAGES
-                                       : ((232448 - 1024 - 256) / kStageBytes);
-    // one C_ij partial of the column half 0 kept in shared memory (fused
-    // Combine H, whole groups): 128 rows x BN/2 fp32
-    static constexpr int kPartialSmem = kBM * (BN / 2) * 4;
+    // one C_ij partial kept in shared memory (fused Combine H, whole groups):
+    // 128 rows x BN (QF) or BN/2 (column half 0) fp32
+    static constexpr int kPartialSmem = kBM * (QF ? BN : BN / 2) * 4;
+    // as many stages as fit in 227 KB (minus the partial, alignment slack and
+    // barriers), <= LCMA_MAX_STAGES
+    static constexpr int kFree = 232448 - 1024 - 256 - kPartialSmem;
+    static constexpr int kStages = (kFree / kStageBytes) > LCMA_MAX_STAGES ? LCMA_MAX_STAGES
+                                                                           : (kFree / kStageBytes);
     static constexpr int kSmemBytes = kStages * kStageBytes + kPartialSmem + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 enum EpiMode : int { EPI_FUSED = 0, EPI_STORE_H = 1 };
 enum OutType : int { OUT_BF16 = 0, OUT_FP16 = 1, OUT_FP32 = 2 };
 enum UnitRole : int { ROLE_WHOLE = 0, ROLE_OWNER = 1, ROLE_CONTRIB = 2 };
+// Where a whole group keeps a live C_ij partial (fp32, the CTA's 128 x BN
+// slab): epilogue-thread registers, shared memory, or an L2 workspace slot.
+enum PartialHome : int { HOME_REG = -1, HOME_SMEM = -2 };
 
 struct GemmParams {
     // problem / blocking
@@ -104,9 +113,9 @@ struct GemmParams {
     int discard;           // 1: discard.global.L2 partial lines after their last read
     int pace_ns;           // >0: sleep between C_ij updates (spreads epilogue traffic)
     int nslot;             // partial tiles live at once for whole groups (<= m*n)
-    int smem_ij;           // C_ij whose column-half-0 partial lives in shared memory (-1: none)
+    int qslot;             // QF = 0: L2 slot of the column half 1 of the HOME_SMEM partial
+    int8_t home[kMaxMN];   // whole groups: C_ij partial home (HOME_REG, HOME_SMEM, or L2 slot >= 0)
     int8_t rperm[kMaxR];   // product processing order inside a group (t -> r)
-    int8_t pslot[kMaxMN];  // shared partial slot of C_ij for whole groups
     int8_t Wc[kMaxR * kMaxMN];   // W[r][i*n + j]
     uint32_t nzmask[kMaxR];      // bit ij set iff W[r][ij] != 0
     uint8_t dbg_extra[kMaxR];    // diagnostics: (nnz(V_r)-1) << 4 | (nnz(U_r)-1)
@@ -290,17 +299,18 @@ __device__ __forceinline__ void store_c8(const GemmParams& p, long long row, lon
 
 // Partial tile layout: [kBN/4][kBM][4] floats, so that the 32 threads of a
 // warp (32 consecutive rows) touch 512 contiguous bytes per float4 access.
-// Whole groups use the shared slot map pslot (C blocks whose live ranges in
-// the product order do not overlap reuse a tile); split segments keep one
-// tile per C block (they stay live until the owner merges them).
+// Whole groups keep a C_ij partial in registers, shared memory or an L2 slot
+// (GemmParams::home; C blocks whose live ranges in the product order do not
+// overlap share a home); split segments keep one L2 tile per C block (they
+// stay live until the owner merges them).
 // Layout: whole-group slots first, slot-major ([nslot][ctas] tiles, one
 // contiguous L2-persistable region), then the split-segment tiles
 // ([2*ctas][m*n]).
 template <int BN = kBN>
-__device__ __forceinline__ float* partial_tile(const GemmParams& p, int slot, int ij, bool whole) {
+__device__ __forceinline__ float* partial_tile(const GemmParams& p, int slot, int idx, bool whole) {
     const size_t T = (size_t)(kBM * BN);
-    if (whole) return p.P + ((size_t)p.pslot[ij] * gridDim.x + slot) * T;
-    return p.P + ((size_t)p.m * p.n * gridDim.x + (size_t)slot * p.m * p.n + ij) * T;
+    if (whole) return p.P + ((size_t)idx * gridDim.x + slot) * T;     // idx = L2 home slot
+    return p.P + ((size_t)p.m * p.n * gridDim.x + (size_t)slot * p.m * p.n + idx) * T;   // idx = ij
 }
 // Drop the 128-byte L2 lines of a partial tile column range after their last
 // read: dead data is neither written back to DRAM nor occupies L2.  Called by
@@ -326,17 +336,17 @@ __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, unsig
 }
 
 // ------------------------------------------------------------ the kernel
-template <int CG, int BN>
+template <int CG, int BN, int QF = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ GemmParams p) {
-    using C_ = Cfg<CG, BN>;
+    using C_ = Cfg<CG, BN, QF>;
     constexpr int kStages = C_::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    float* psmem = reinterpret_cast<float*>(smem + kStages * C_::kStageBytes);   // [BN/8][kBM][4]
+    float* psmem = reinterpret_cast<float*>(smem + kStages * C_::kStageBytes);   // [QF?BN/4:BN/8][kBM][4]
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * C_::kStageBytes + C_::kPartialSmem);
     uint64_t* empty_bar = full_bar + kStages;
     uint64_t* tfull_bar = empty_bar + kStages;   // [2]
@@ -375,11 +385,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // registers: the TMA / MMA / allocator warpgroup needs few, the two
+    // epilogue warpgroups keep a 128 x BN fp32 partial (BN/2 per thread)
+    // in registers on top of the H chunk (128*56 + 256*224 = 384*168).
+    // Each role branch starts with its setmaxnreg so that ptxas allocates
+    // the branch with that budget.
 
     const int w = blockIdx.x / CG;           // work-unit slot (pair index for CG = 2)
 
     if (warp == 0) {
         // ================================ TMA producer (both CTAs of a pair)
+        ptx::setmaxnreg_dec<56>();
         if (ptx::elect_one()) {
             const int b_bytes_chunk = p.BK * 128;   // MN-major chunk: BK rows x 128 B
             const int n_chunks = C_::kBNc / p.BK;   // MN-major: 128-byte column chunks per CTA
@@ -467,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // The whole warp walks the schedule so that stage / descriptor
         // arithmetic stays in uniform registers; one lane issues the MMAs and
         // the commits (a commit tracks the MMAs of the issuing thread).
+        ptx::setmaxnreg_dec<56>();
         if (leader) {
             const uint32_t b_lbo = p.BK * 128;            // MN-major: chunk stride
             const uint32_t b_kstep = p.b_mn_major ? (uint32_t)(32 / (p.tf32 ? 4 : 2)) * 128u : 32u;
@@ -541,8 +558,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 p.stats[blockIdx.x * 8 + 3] = (unsigned long long)(clock64() - t_start);
             }
         }
-    } else if (warp >= kEpiWarp0) {
+    } else if (warp < kEpiWarp0) {
+        ptx::setmaxnreg_dec<56>();   // allocator / idle warps
+    } else {
         // ================================ epilogue (both CTAs: own 128 rows)
+        ptx::setmaxnreg_inc<224>();
         const int ew = warp - kEpiWarp0;           // 0..7
         const int quarter = warp & 3;              // TMEM lane quarter
         const int half = ew >> 2;                  // column half
@@ -555,6 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             CG == 2 ? ptx::mapa_shared(ptx::smem_u32(&tempty_bar[0]), 0) : 0u;
         int acc = 0;
         uint32_t acc_phase = 0;
+        float preg[BN / 2];       // HOME_REG partial: (row, this thread's column half)
         UnitIter it(p, w);
         Unit u;
         while (it.next(u)) {
@@ -576,136 +597,162 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t t_addr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
                                         (uint32_t)(acc * BN + half * (BN / 2));
-                // drain this thread's 128 accumulator columns, then release the
-                // accumulator to the MMA warp before any global-memory traffic
-                uint32_t raw[BN / 2];
-                if (!(p.debug & 2)) {
-#pragma unroll
-                    for (int ch = 0; ch < (BN / 2) / 32; ++ch)
-                        ptx::tmem_ld_32x32b_x32(t_addr + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(&raw[ch * 32]));
-                    ptx::tmem_wait_ld();
-                }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
-                    else ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
-                }
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-                if (p.debug & 1) continue;
-                const int col_base = half * (BN / 2);
-                if (p.epi_mode == EPI_STORE_H) {
-                    // Algorithm 1 stage 3: H_r to main memory
-                    float* dst = p.H + ((long long)r * p.Mb + brow) * p.Nb + (long long)z * BN + col_base;
-#pragma unroll
-                    for (int e = 0; e < BN / 2; e += 4)
-                        st_cg_f4(dst + e, make_float4(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1]),
-                                                      __uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])));
-                    continue;
-                }
-                // Combine H (Eq. 6): C_ij += W[r,i,j] * H_r for every nonzero W
                 const uint32_t nz = p.nzmask[r];
-                for (int ij = 0; ij < mn; ++ij) {
-                    if (!((nz >> ij) & 1u)) continue;
-                    const float sw = (float)p.Wc[r * mn + ij];
-                    float* pt = partial_tile<BN>(p, slot, ij, whole);
-                    const bool first = !((seen >> ij) & 1u);
-                    const bool final_here = whole && !((later >> ij) & 1u);
-                    if (whole && ij == p.smem_ij && half == 0) {
-                        // shared-memory partial: this thread alone owns (row, cols
-                        // 0..BN/2-1) of it, so plain loads/stores in program order
-                        float* sp = psmem;
-                        if (final_here) {
-                            const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
-                            const long long ccol0 = (long long)j * p.Nb + (long long)z * BN;
-                            const bool in_range = brow < p.Mb && ccol0 < (long long)(j + 1) * p.Nb;
-#pragma unroll
-                            for (int ch = 0; ch < (BN / 2) / 32; ++ch) {
-                                float v[32];
-#pragma unroll
-                                for (int e = 0; e < 32; e += 4) {
-                                    float4 o = first ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                                     : *reinterpret_cast<const float4*>(sp + partial_off(row, (ch * 32 + e) >> 2));
-                                    v[e] = o.x + sw * __uint_as_float(raw[ch * 32 + e]);
-                                    v[e + 1] = o.y + sw * __uint_as_float(raw[ch * 32 + e + 1]);
-                                    v[e + 2] = o.z + sw * __uint_as_float(raw[ch * 32 + e + 2]);
-                                    v[e + 3] = o.w + sw * __uint_as_float(raw[ch * 32 + e + 3]);
-                                }
-                                if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol0 + ch * 32, v);
-                            }
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < BN / 2; e += 4) {
-                                float4* q = reinterpret_cast<float4*>(sp + partial_off(row, e >> 2));
-                                float4 o = first ? make_float4(0.f, 0.f, 0.f, 0.f) : *q;
-                                o.x += sw * __uint_as_float(raw[e]);
-                                o.y += sw * __uint_as_float(raw[e + 1]);
-                                o.z += sw * __uint_as_float(raw[e + 2]);
-                                o.w += sw * __uint_as_float(raw[e + 3]);
-                                *q = o;
-                            }
-                        }
-                    } else if (final_here) {
-                        // last contribution: C_ij = partial + w*H_r, rounded once.
-                        // 32 columns per step: the 8 partial loads are issued
-                        // together (one L2 round trip per step, not per vector)
-                        const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
-                        const long long ccol0 = (long long)j * p.Nb + (long long)z * BN + col_base;
-                        const bool in_range = brow < p.Mb && ccol0 < (long long)(j + 1) * p.Nb;
-#pragma unroll
-                        for (int ch = 0; ch < (BN / 2) / 32; ++ch) {
-                            float v[32];
-#pragma unroll
-                            for (int e = 0; e < 32; ++e) v[e] = sw * __uint_as_float(raw[ch * 32 + e]);
-                            if (!first) {
-                                float4 o[8];
-#pragma unroll
-                                for (int q = 0; q < 8; ++q)
-                                    o[q] = ld_cg_f4(pt + partial_off(row, (col_base + ch * 32 + 4 * q) >> 2));
-#pragma unroll
-                                for (int q = 0; q < 8; ++q) {
-                                    v[4 * q] += o[q].x; v[4 * q + 1] += o[q].y;
-                                    v[4 * q + 2] += o[q].z; v[4 * q + 3] += o[q].w;
-                                }
-                            }
-                            if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol0 + ch * 32, v);
-                        }
-                        if (!first && p.discard) {
-                            __syncwarp();      // the 8 lanes sharing a line have read it
-                            if ((row & 7) == 0) discard_lines(pt, row, col_base >> 2, BN / 8);
-                        }
-                    } else if (first) {
-                        if (p.partial_hint) {
-#pragma unroll
-                            for (int e = 0; e < BN / 2; e += 4)
-                                st_pol_f4(pt + partial_off(row, (col_base + e) >> 2),
-                                          make_float4(sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
-                                                      sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3])),
-                                          pol);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < BN / 2; e += 4)
-                                st_cg_f4(pt + partial_off(row, (col_base + e) >> 2),
-                                         make_float4(sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
-                                                     sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3])));
-                        }
-                    } else if (p.partial_hint) {
-#pragma unroll
-                        for (int e = 0; e < BN / 2; e += 4)
-                            red_add_pol_f4(pt + partial_off(row, (col_base + e) >> 2),
-                                           sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
-                                           sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3]), pol);
+                // destinations whose last contribution this is come first: a
+                // home they free may be taken by a first contribution of the
+                // same product (each thread touches only its own elements)
+                const uint32_t fin = whole ? (nz & ~later) : 0u;
+                const int col_base = half * (BN / 2);
+                // the accumulator is consumed in chunks of 32 columns; it is
+                // released to the MMA warp right after the last chunk's load.
+                // The chunk index is a template constant so that the register
+                // partial preg is indexed statically (stays in registers).
+                auto chunk = [&](auto ch_c) {
+                    constexpr int ch = decltype(ch_c)::value;
+                    uint32_t raw[32];
+                    if (!(p.debug & 2)) {
+                        ptx::tmem_ld_32x32b_x32(t_addr + ch * 32, raw);
+                        ptx::tmem_wait_ld();
                     } else {
-                        // middle contribution: fire-and-forget L2 reduction (same
-                        // thread, same address => applied in program order)
 #pragma unroll
-                        for (int e = 0; e < BN / 2; e += 4)
-                            red_add_f4(pt + partial_off(row, (col_base + e) >> 2),
-                                       sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
-                                       sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3]));
+                        for (int e = 0; e < 32; ++e) raw[e] = 0u;
+                    }
+                    if (ch == (BN / 2) / 32 - 1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
+                            else ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+                        }
+                    }
+                    if (p.debug & 1) return;
+                    const int c4 = (col_base + ch * 32) >> 2;     // first float4 column of the chunk
+                    if (p.epi_mode == EPI_STORE_H) {
+                        // Algorithm 1 stage 3: H_r to main memory
+                        float* dst = p.H + ((long long)r * p.Mb + brow) * p.Nb + (long long)z * BN + col_base + ch * 32;
+#pragma unroll
+                        for (int e = 0; e < 32; e += 4)
+                            st_cg_f4(dst + e, make_float4(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1]),
+                                                          __uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])));
+                        return;
+                    }
+                    // Combine H (Eq. 6): C_ij += W[r,i,j] * H_r for every nonzero W
+                    for (int pass = 0; pass < 2; ++pass) {
+                        uint32_t todo = pass == 0 ? fin : (nz & ~fin);
+                        while (todo) {
+                            const int ij = __ffs(todo) - 1;
+                            todo &= todo - 1;
+                            const float sw = (float)p.Wc[r * mn + ij];
+                            const bool first = !((seen >> ij) & 1u);
+                            const bool final_here = pass == 0;
+                            int home = whole ? (int)p.home[ij] : 0;
+                            if (QF == 0 && home == HOME_SMEM && half == 1) home = p.qslot;
+                            const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
+                            const long long ccol = (long long)j * p.Nb + (long long)z * BN + col_base + ch * 32;
+                            const bool in_range = brow < p.Mb && ccol < (long long)(j + 1) * p.Nb;
+                            if (whole && home == HOME_REG) {
+                                float* pr = &preg[ch * 32];
+                                if (final_here) {
+                                    float v[32];
+#pragma unroll
+                                    for (int e = 0; e < 32; ++e)
+                                        v[e] = (first ? 0.f : pr[e]) + sw * __uint_as_float(raw[e]);
+                                    if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
+                                } else if (first) {
+#pragma unroll
+                                    for (int e = 0; e < 32; ++e) pr[e] = sw * __uint_as_float(raw[e]);
+                                } else {
+#pragma unroll
+                                    for (int e = 0; e < 32; ++e) pr[e] += sw * __uint_as_float(raw[e]);
+                                }
+                            } else if (whole && home == HOME_SMEM) {
+                                // this thread alone owns (row, its column half) of the
+                                // shared partial: plain loads / stores in program order
+                                float* sp = psmem;
+                                if (final_here) {
+                                    float v[32];
+#pragma unroll
+                                    for (int e = 0; e < 32; e += 4) {
+                                        float4 o = first ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                         : *reinterpret_cast<const float4*>(sp + partial_off(row, c4 + (e >> 2)));
+                                        v[e] = o.x + sw * __uint_as_float(raw[e]);
+                                        v[e + 1] = o.y + sw * __uint_as_float(raw[e + 1]);
+                                        v[e + 2] = o.z + sw * __uint_as_float(raw[e + 2]);
+                                        v[e + 3] = o.w + sw * __uint_as_float(raw[e + 3]);
+                                    }
+                                    if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
+                                } else {
+#pragma unroll
+                                    for (int e = 0; e < 32; e += 4) {
+                                        float4* q = reinterpret_cast<float4*>(sp + partial_off(row, c4 + (e >> 2)));
+                                        float4 o = first ? make_float4(0.f, 0.f, 0.f, 0.f) : *q;
+                                        o.x += sw * __uint_as_float(raw[e]);
+                                        o.y += sw * __uint_as_float(raw[e + 1]);
+                                        o.z += sw * __uint_as_float(raw[e + 2]);
+                                        o.w += sw * __uint_as_float(raw[e + 3]);
+                                        *q = o;
+                                    }
+                                }
+                            } else {
+                                // L2 workspace slot
+                                float* pt = whole ? partial_tile<BN>(p, slot, home, true)
+                                                  : partial_tile<BN>(p, slot, ij, false);
+                                if (final_here) {
+                                    // last contribution: C_ij = partial + w*H_r, rounded once;
+                                    // the 8 partial loads are issued together
+                                    float v[32];
+#pragma unroll
+                                    for (int e = 0; e < 32; ++e) v[e] = sw * __uint_as_float(raw[e]);
+                                    if (!first) {
+                                        float4 o[8];
+#pragma unroll
+                                        for (int q = 0; q < 8; ++q) o[q] = ld_cg_f4(pt + partial_off(row, c4 + q));
+#pragma unroll
+                                        for (int q = 0; q < 8; ++q) {
+                                            v[4 * q] += o[q].x; v[4 * q + 1] += o[q].y;
+                                            v[4 * q + 2] += o[q].z; v[4 * q + 3] += o[q].w;
+                                        }
+                                    }
+                                    if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
+                                    if (!first && p.discard) {
+                                        __syncwarp();      // the 8 lanes sharing a line have read it
+                                        if ((row & 7) == 0) discard_lines(pt, row, c4, 8);
+                                    }
+                                } else if (first) {
+#pragma unroll
+                                    for (int e = 0; e < 32; e += 4) {
+                                        const float4 hv = make_float4(sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
+                                                                      sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3]));
+                                        if (p.partial_hint) st_pol_f4(pt + partial_off(row, c4 + (e >> 2)), hv, pol);
+                                        else st_cg_f4(pt + partial_off(row, c4 + (e >> 2)), hv);
+                                    }
+                                } else {
+                                    // middle contribution: fire-and-forget L2 reduction (same
+                                    // thread, same address => applied in program order)
+#pragma unroll
+                                    for (int e = 0; e < 32; e += 4) {
+                                        float* a = pt + partial_off(row, c4 + (e >> 2));
+                                        if (p.partial_hint)
+                                            red_add_pol_f4(a, sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
+                                                           sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3]), pol);
+                                        else
+                                            red_add_f4(a, sw * __uint_as_float(raw[e]), sw * __uint_as_float(raw[e + 1]),
+                                                       sw * __uint_as_float(raw[e + 2]), sw * __uint_as_float(raw[e + 3]));
+                                    }
+                                }
+                            }
+                        }
                     }
                     if (p.pace_ns) __nanosleep(p.pace_ns);   // spread the epilogue's L2 traffic
+                };
+                static_assert((BN / 2) / 32 == 4 || (BN / 2) / 32 == 2, "chunks per column half");
+                chunk(std::integral_constant<int, 0>{});
+                chunk(std::integral_constant<int, 1>{});
+                if constexpr ((BN / 2) / 32 == 4) {
+                    chunk(std::integral_constant<int, 2>{});
+                    chunk(std::integral_constant<int, 3>{});
                 }
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 seen |= nz;
             }
             if (p.epi_mode != EPI_FUSED || u.role == ROLE_WHOLE || (p.debug & 1)) continue;

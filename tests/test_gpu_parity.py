@@ -72,7 +72,7 @@ def test_two_level_exact(shape, b_layout):
     # Strassen^2 as Strassen o Strassen: inner fused GEMMs write the outer H_q
     # in fp32, the outer Combine H runs as an HBM pass (LCMA_VARIANT_TWO_LEVEL)
     plan = _exact_case(*shape, "strassen2", b_layout=b_layout, variant="two_level")
-    assert plan.info["variant"] == L.VARIANT["two_level"] and plan.info["partial_slots"] == 3
+    assert plan.info["variant"] == L.VARIANT["two_level"] and plan.info["partial_slots"] == 2
 
 
 def test_two_level_float_and_static_b():
