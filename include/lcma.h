@@ -184,6 +184,11 @@ void lcma_set_kernel_events(void* ev_start, void* ev_end);
 /* Diagnostics (LCMA_STATS=1 in the environment): copies n per-CTA wait-cycle
  * counters to host memory; returns 0 on success. */
 int lcma_debug_stats(unsigned long long* host, int n);
+/* Diagnostics (host only): fused Combine-H partial tile transfers per group
+ * that still go through L2 once the two most-updated partial slots live on
+ * chip (epilogue registers; shared memory for column half 0), for a scheme
+ * id; *live (if non-NULL) receives the partials live at once per CTA. */
+double lcma_debug_l2_partial_tiles(int32_t scheme_id, int32_t* live);
 
 /* Thread-local message for the last error on this thread ("" if none). */
 const char* lcma_last_error(void);

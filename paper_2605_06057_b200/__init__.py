@@ -14,7 +14,8 @@ __all__ = ["lib", "Plan", "decide", "scheme_get", "scheme_register_file", "schem
            "LcmaError", "BF16", "FP16", "TF32", "FP32", "ALGO", "VARIANT"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liblcma.so")
+# LCMA_LIB: an alternative build of the same library (tuning experiments)
+_LIB_PATH = os.environ.get("LCMA_LIB") or os.path.join(_HERE, "liblcma.so")
 
 BF16, FP16, TF32, FP32 = 0, 1, 2, 3
 ALGO = {"auto": 0, "classical": 1, "strassen": 2, "strassen2": 3, "laderman": 4, "scheme": 5}

@@ -24,10 +24,10 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB) -> str:
+    if out == LIB and not force and not _stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-cudart", "static", "-I", os.path.join(HERE, "..", "include"),
            "-Xptxas", "-v" if verbose else "-O3",
@@ -35,10 +35,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    # --out PATH: build a variant (e.g. with LCMA_NVCC_FLAGS) beside the
+    # in-tree library, loaded with LCMA_LIB=PATH for tuning experiments
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else LIB
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=out))

@@ -74,11 +74,13 @@ double condition_lhs(const Scheme& s, double M, double N, double K, bool fused) 
 //    beta_combine (they are HBM-latency bound, not at copy bandwidth);
 //  * the GEMM stage runs at the measured classical-kernel throughput FLOPS_x
 //    on the tile-rounded extents;
-//  * the fused Combine H (C_ij partials in L2) slows the mainloop by
-//    alpha * rho^2, rho = (partial bytes written/read per product) /
-//    (operand bytes loaded per product) -- fitted on Strassen, Laderman and
-//    Strassen^2 at cfg2 (profiles/); the unfused variant instead pays an
-//    HBM pass over H (R*Mb*Nb*4 + M*N*e bytes) at beta.
+//  * the fused Combine H keeps the two most-updated C_ij partial slots on
+//    chip (registers; shared memory for column half 0); the GEMM stage costs
+//    t_mma * (1 + epi_overhead + alpha * rho^2), rho = (partial bytes still
+//    moved through L2 per product) / (operand bytes per product), both per
+//    CTA -- fitted on the cfg3 sweep (profiles/r01f_cfg3_decision.json); the
+//    unfused variant instead pays an HBM pass over H (R*Mb*Nb*4 + M*N*e
+//    bytes) at beta.
 double estimate_time_b200(const Scheme& s, double M, double N, double K, const Profile& hw,
                           bool fused, bool b_static, double elem_bytes) {
     const double R = s.R;
@@ -91,21 +93,11 @@ double estimate_time_b200(const Scheme& s, double M, double N, double K, const P
     if (!b_static) t += (K * N + R * Kb * Nb) / hw.beta_combine;        // Combine B
     const double t_mma = 2.0 * R * Mb * Nb * Kb / hw.flops_mul;         // R sub-GEMMs
     if (fused) {
-        const double contrib = (double)s.nnzW() / R;                     // C_ij updates per product
-        const double partial = contrib * 128.0 * tileN * 4.0;           // fp32 partial bytes per CTA
-        const double operand = (Kb / BK) * (128.0 * 128.0 + 128.0 * 128.0);   // A + B half per CTA
+        const double l2_tiles = scheme_product_order(s.id).l2_tiles;   // partial tile transfers per CTA and group
+        const double partial = l2_tiles * 128.0 * tileN * 4.0;          // fp32 partial bytes per CTA and group
+        const double operand = R * (Kb / BK) * (128.0 * 128.0 + 128.0 * 128.0);   // A + B half per CTA and group
         const double rho = partial / operand;
-        t += t_mma * (1.0 + hw.alpha_partial * rho * rho);
-        // live partial tiles of all CTAs beyond the L2 budget spill to HBM:
-        // every C_ij update then costs an HBM round trip of the fp32 tile
-        const int nslot = scheme_product_order(s.id).nslot;
-        const double footprint = (double)nslot * 128.0 * tileN * 4.0 * 148.0;
-        if (footprint > hw.l2_partial_budget) {
-            const double groups = (Mb / tileM) * (Nb / tileN);
-            const double tile_bytes = tileM * tileN * 4.0;
-            const double bytes = groups * ((double)s.nnzW() + (double)s.m * s.n) * tile_bytes;
-            t += bytes / (hw.beta * elem_bytes);
-        }
+        t += t_mma * (1.0 + hw.epi_overhead + hw.alpha_partial * rho * rho);
     } else {
         t += t_mma + (R * Mb * Nb * 4.0 + M * N * elem_bytes) / (hw.beta * elem_bytes);
     }
@@ -166,9 +158,11 @@ Profile default_profile(int dtype) {
     p.beta = 6.55e12 / bytes;
     // group_combine_kernel measured ~4.4 TB/s of read+write traffic (cfg2)
     p.beta_combine = 4.4e12 / bytes;
-    // fused Combine-H mainloop slowdown coefficient (fit: Strassen 0.276 at
-    // rho 0.214, Laderman 1.08 at 0.404, Strassen^2 2.39 at 0.735)
-    p.alpha_partial = 6.0;
+    // fused Combine H with on-chip partial homes (fit on the cfg3 sweep,
+    // profiles/r01f_cfg3_decision.json: Strassen median overhead +8 % for
+    // 16-bit data and -4 % for tf32, Laderman / Strassen^2 through alpha)
+    p.alpha_partial = 8.0;
+    p.epi_overhead = bytes == 2.0 ? 0.08 : -0.04;
     if (const char* env = std::getenv("LCMA_PROFILE")) {
         const char* keys[5] = {"flops_mul=", "flops_add=", "beta_elems=", "beta_combine=", "alpha_partial="};
         double* dst[5] = {&p.flops_mul, &p.flops_add, &p.beta, &p.beta_combine, &p.alpha_partial};

@@ -15,8 +15,8 @@ struct Profile {
     double beta;        // off-chip bandwidth, elements/s of the dtype
     // B200-calibrated model only (decide_b200):
     double beta_combine = 0.0;    // combine kernels' element rate (elements/s)
-    double alpha_partial = 0.0;   // fused Combine-H mainloop slowdown coefficient
-    double l2_partial_budget = 64.0 * 1024 * 1024;   // L2 bytes the live partial tiles may use
+    double alpha_partial = 0.0;   // fused Combine-H slowdown per (L2 partial / operand bytes)^2
+    double epi_overhead = 0.0;    // fused GEMM time over R/mnk of the classical kernel's, on-chip part
 };
 
 struct StageCost {

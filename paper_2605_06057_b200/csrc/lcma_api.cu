@@ -196,6 +196,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         Profile def = default_profile((int)d.dtype);
         p->hw.beta_combine = def.beta_combine * (p->hw.beta / def.beta);
         p->hw.alpha_partial = def.alpha_partial;
+        p->hw.epi_overhead = def.epi_overhead;
     }
     DecisionResult dec = paper_model
         ? decide(cands, (double)d.M, (double)d.N, (double)d.K, p->hw, fused_model, d.b_static != 0)
@@ -818,10 +819,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         for (int t = 0; t < S.R; ++t) g.rperm[t] = (int8_t)po.perm[t];
         // slot -> home
         const int ns = po.nslot;
-        std::vector<int> by_use(ns);
-        for (int k = 0; k < ns; ++k) by_use[k] = k;
-        std::stable_sort(by_use.begin(), by_use.end(),
-                         [&](int a, int b) { return po.slot_updates[a] > po.slot_updates[b]; });
+        const std::vector<int>& by_use = po.by_use;
         const bool use_reg = !H && !(std::getenv("LCMA_REG_PARTIAL") && std::atoi(std::getenv("LCMA_REG_PARTIAL")) == 0);
         const bool use_smem = !H && !(std::getenv("LCMA_SMEM_PARTIAL") && std::atoi(std::getenv("LCMA_SMEM_PARTIAL")) == 0);
         std::vector<int> slot_home(ns, 0);
@@ -839,6 +837,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         g.qslot = 0;
         g.nslot = mn;
     }
+    g.serpentine = 0;
+    if (const char* v = std::getenv("LCMA_SERPENTINE")) g.serpentine = std::atoi(v);
     g.discard = 1;
     if (const char* dc = std::getenv("LCMA_DISCARD")) g.discard = std::atoi(dc);
     if (const char* pn = std::getenv("LCMA_PACE_NS")) g.pace_ns = std::atoi(pn);
@@ -1051,6 +1051,14 @@ extern "C" void lcma_set_kernel_events(void* ev_start, void* ev_end) {
 
 // Diagnostics: co-resident clusters of `cluster_size` CTAs for the tcgen05
 // GEMM kernel configuration (cudaOccupancyMaxActiveClusters); -1 on error.
+// Diagnostics: fused Combine-H partial tile transfers per group that go to L2
+// (the on-chip homes excluded) and live partials per CTA, for scheme_id.
+extern "C" double lcma_debug_l2_partial_tiles(int32_t scheme_id, int32_t* live) {
+    const ProductOrder& po = scheme_product_order(scheme_id);
+    if (live) *live = po.nslot;
+    return po.l2_tiles;
+}
+
 extern "C" int lcma_debug_max_clusters(int cluster_size) {
     if (cudaFuncSetAttribute(umma_gemm_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg<2, 256>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return -1; }

@@ -148,6 +148,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_b
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
+// Relaxed arrive: no ordering of the caller's earlier global / shared memory
+// operations (a release arrive at cluster scope waits for all outstanding
+// stores: MEMBAR.GPU + ERRBAR).  Used where the arrival only reports that
+// TMEM reads have completed (tcgen05.wait::ld + tcgen05.fence::before).
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_bar) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // 2-SM TMA: data lands in this CTA's smem, transaction bytes are counted on
 // the barrier at shared::cluster address `cluster_bar` (the pair leader's).
 // 3-D tile loads (MN-major B: {128-byte column chunk, K row, chunk index}).

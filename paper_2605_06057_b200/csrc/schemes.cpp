@@ -398,11 +398,22 @@ ProductOrder compute_order(const Scheme& s) {
             chosen = (int)slot_end.size();
             slot_end.push_back(-1);
             o.slot_updates.push_back(0);
+            o.slot_access.push_back(0);
         }
         slot_end[chosen] = last[ij];
         o.slot_updates[chosen] += uses[ij] - 1;   // stored partial accesses (all but the first's store)
+        o.slot_access[chosen] += uses[ij];        // tile transfers if the slot lived in L2
         o.slot[ij] = chosen;
     }
+    // home ranking: most-updated slots first (registers, then shared memory)
+    const int ns = (int)slot_end.size();
+    o.by_use.resize(ns);
+    for (int k = 0; k < ns; ++k) o.by_use[k] = k;
+    std::stable_sort(o.by_use.begin(), o.by_use.end(),
+                     [&](int a, int b) { return o.slot_updates[a] > o.slot_updates[b]; });
+    o.l2_tiles = 0.0;
+    for (int k = 0; k < ns; ++k)
+        o.l2_tiles += k == 0 ? 0.0 : k == 1 ? 0.5 * o.slot_access[o.by_use[k]] : (double)o.slot_access[o.by_use[k]];
     o.nslot = (int)slot_end.size();
     return o;
 }

@@ -46,6 +46,10 @@ struct ProductOrder {
     std::vector<int> perm;           // position t -> product r
     std::vector<int> slot;           // C_ij -> slot (-1: one contribution, never stored)
     std::vector<int> slot_updates;   // per slot: partial read-modify-writes over a group
+    std::vector<int> slot_access;    // per slot: partial tile transfers over a group if homed in L2
+    std::vector<int> by_use;         // slots by decreasing updates: [0] -> registers, [1] -> shared memory
+    double l2_tiles = 0.0;           // partial tile transfers per group that still go to L2 (the
+                                     // shared-memory home holds column half 0 only)
     int nslot = 0;                   // partials live at once (per CTA)
     int max_live = 0;
 };

@@ -35,7 +35,7 @@
 namespace lcma {
 
 #ifndef LCMA_MAX_STAGES
-#define LCMA_MAX_STAGES 4         // smem ring depth (measured best: 4 > 5 > 6 > 7 > 3)
+#define LCMA_MAX_STAGES 5         // smem ring depth (on-chip partial homes: 5 >= 4; earlier kernel: 4 > 5 > 6 > 7 > 3)
 #endif
 constexpr int kBM = 128;          // rows per CTA (TMEM lanes)
 constexpr int kBN = 256;          // UMMA N = accumulator columns
@@ -113,6 +113,7 @@ struct GemmParams {
     int discard;           // 1: discard.global.L2 partial lines after their last read
     int pace_ns;           // >0: sleep between C_ij updates (spreads epilogue traffic)
     int nslot;             // partial tiles live at once for whole groups (<= m*n)
+    int serpentine;        // odd lockstep rounds process their products in reverse order
     int qslot;             // QF = 0: L2 slot of the column half 1 of the HOME_SMEM partial
     int8_t home[kMaxMN];   // whole groups: C_ij partial home (HOME_REG, HOME_SMEM, or L2 slot >= 0)
     int8_t rperm[kMaxR];   // product processing order inside a group (t -> r)
@@ -124,6 +125,7 @@ struct GemmParams {
 // ------------------------------------------------------------ scheduling
 struct Unit {
     int g, r0, r1, role;
+    int rev;             // whole group of an odd lockstep round: products in reverse order
 };
 
 // Enumerates the units of work-unit slot `w` in processing order.  Every role
@@ -149,6 +151,10 @@ struct UnitIter {
             u.r0 = 0;
             u.r1 = p.R;
             u.role = ROLE_WHOLE;
+            // serpentine product order over rounds: a round starts with the
+            // product the previous round ended with (its operand panels are
+            // still in L2)
+            u.rev = p.serpentine ? (idx & 1) : 0;
             ++idx;
             return true;
         }
@@ -162,10 +168,16 @@ struct UnitIter {
         u.r0 = r0;
         u.r1 = r1;
         u.role = (r0 == 0 && r1 == p.R) ? ROLE_WHOLE : (r0 == 0 ? ROLE_OWNER : ROLE_CONTRIB);
+        u.rev = 0;
         t = stop;
         return true;
     }
 };
+
+// Product processed at position t of unit u.
+__device__ __forceinline__ int product_at(const GemmParams& p, const Unit& u, int t) {
+    return p.rperm[u.rev ? p.R - 1 - t : t];
+}
 
 // Group index -> tile coordinates: bands of `swz` tile-rows traversed
 // column by column so that the W groups of a lockstep round cover a compact
@@ -411,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int x, z;
                 group_xz(p, u.g, x, z);
                 for (int t = u.r0; t < u.r1; ++t) {
-                    const int r = p.rperm[t];
+                    const int r = product_at(p, u, t);
                     const int a_row = r * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
                     const int b_col0 = z * BN + (int)rank * C_::kBNc;
                     for (int kb = 0; kb < p.nK; ++kb) {
@@ -588,10 +600,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int slot = (u.role == ROLE_CONTRIB) ? (int)gridDim.x + (int)blockIdx.x : (int)blockIdx.x;
             const bool whole = u.role == ROLE_WHOLE;
             for (int t = u.r0; t < u.r1; ++t) {
-                const int r = p.rperm[t];
+                const int r = product_at(p, u, t);
                 // C_ij that later products of this unit still update
                 uint32_t later = 0;
-                for (int t2 = t + 1; t2 < u.r1; ++t2) later |= p.nzmask[p.rperm[t2]];
+                for (int t2 = t + 1; t2 < u.r1; ++t2) later |= p.nzmask[product_at(p, u, t2)];
                 if (p.debug & 8) ptx::mbar_wait_sleep(&tfull_bar[acc], acc_phase, 256);
                 else timed_wait(&tfull_bar[acc], acc_phase, (p.stats && ew == 0 && lane == 0) ? &w_tfull : nullptr);
                 ptx::tc_fence_after();
@@ -618,11 +630,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int e = 0; e < 32; ++e) raw[e] = 0u;
                     }
                     if (ch == (BN / 2) / 32 - 1) {
+                        // relaxed: the arrival must not wait for this product's
+                        // earlier C / partial stores to complete
                         ptx::tc_fence_before();
                         __syncwarp();
                         if (lane == 0) {
-                            if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
-                            else ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+                            if constexpr (CG == 1) ptx::mbar_arrive_relaxed(&tempty_bar[acc]);
+                            else ptx::mbar_arrive_cluster_relaxed(tempty_leader0 + acc * 8);
                         }
                     }
                     if (p.debug & 1) return;
