@@ -135,11 +135,11 @@ struct UnitIter {
     const GemmParams& p;
     int w;
     int idx;             // lockstep round index, then tail
-    long long t, t_end;  // tail tile cursor
+    int t, t_end;        // tail tile cursor (G * R < 2^31)
     __device__ UnitIter(const GemmParams& p_, int w_) : p(p_), w(w_), idx(0) {
-        long long Tt = (long long)(p.G - p.q * p.W) * p.R;
+        int Tt = (p.G - p.q * p.W) * p.R;
         if (Tt < 0) Tt = 0;
-        t = (long long)w * p.tail_c;
+        t = w * p.tail_c;
         t_end = t + p.tail_c;
         if (t_end > Tt) t_end = Tt;
         if (t > Tt) t = Tt;
@@ -159,9 +159,9 @@ struct UnitIter {
             return true;
         }
         if (t >= t_end) return false;
-        long long gl = t / p.R;                // tail-local group
+        int gl = t / p.R;                // tail-local group
         int r0 = (int)(t - gl * p.R);
-        long long stop = (gl + 1) * p.R;
+        int stop = (gl + 1) * p.R;
         if (stop > t_end) stop = t_end;
         int r1 = (int)(stop - gl * p.R);
         u.g = p.q * p.W + (int)gl;
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ================================ TMA producer (both CTAs of a pair)
-        ptx::setmaxnreg_dec<56>();
+        ptx::setmaxnreg_dec<40>();
         if (ptx::elect_one()) {
             const int b_bytes_chunk = p.BK * 128;   // MN-major chunk: BK rows x 128 B
             const int n_chunks = C_::kBNc / p.BK;   // MN-major: 128-byte column chunks per CTA
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // The whole warp walks the schedule so that stage / descriptor
         // arithmetic stays in uniform registers; one lane issues the MMAs and
         // the commits (a commit tracks the MMAs of the issuing thread).
-        ptx::setmaxnreg_dec<56>();
+        ptx::setmaxnreg_dec<40>();
         if (leader) {
             const uint32_t b_lbo = p.BK * 128;            // MN-major: chunk stride
             const uint32_t b_kstep = p.b_mn_major ? (uint32_t)(32 / (p.tf32 ? 4 : 2)) * 128u : 32u;
@@ -571,10 +571,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp < kEpiWarp0) {
-        ptx::setmaxnreg_dec<56>();   // allocator / idle warps
+        ptx::setmaxnreg_dec<40>();   // allocator / idle warps
     } else {
         // ================================ epilogue (both CTAs: own 128 rows)
-        ptx::setmaxnreg_inc<224>();
+        ptx::setmaxnreg_inc<232>();
         const int ew = warp - kEpiWarp0;           // 0..7
         const int quarter = warp & 3;              // TMEM lane quarter
         const int half = ew >> 2;                  // column half
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // released to the MMA warp right after the last chunk's load.
                 // The chunk index is a template constant so that the register
                 // partial preg is indexed statically (stays in registers).
-                auto chunk = [&](auto ch_c) {
+                auto chunk = [=, &preg, &p](auto ch_c) {
                     constexpr int ch = decltype(ch_c)::value;
                     uint32_t raw[32];
                     if (!(p.debug & 2)) {
@@ -665,13 +665,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const long long ccol = (long long)j * p.Nb + (long long)z * BN + col_base + ch * 32;
                             const bool in_range = brow < p.Mb && ccol < (long long)(j + 1) * p.Nb;
                             if (whole && home == HOME_REG) {
+                                if (p.debug & 1024) continue;
                                 float* pr = &preg[ch * 32];
                                 if (final_here) {
-                                    float v[32];
+                                    // the partial dies here: finish C in place (no extra
+                                    // 32-register buffer; a first contribution of this
+                                    // product into the same home comes after)
 #pragma unroll
                                     for (int e = 0; e < 32; ++e)
-                                        v[e] = (first ? 0.f : pr[e]) + sw * __uint_as_float(raw[e]);
-                                    if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
+                                        pr[e] = (first ? 0.f : pr[e]) + sw * __uint_as_float(raw[e]);
+                                    if (in_range && !(p.debug & 128)) store_c_row(p, (long long)i * p.Mb + brow, ccol, pr);
                                 } else if (first) {
 #pragma unroll
                                     for (int e = 0; e < 32; ++e) pr[e] = sw * __uint_as_float(raw[e]);
@@ -680,6 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     for (int e = 0; e < 32; ++e) pr[e] += sw * __uint_as_float(raw[e]);
                                 }
                             } else if (whole && home == HOME_SMEM) {
+                                if (p.debug & 512) continue;
                                 // this thread alone owns (row, its column half) of the
                                 // shared partial: plain loads / stores in program order
                                 float* sp = psmem;
@@ -694,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         v[e + 2] = o.z + sw * __uint_as_float(raw[e + 2]);
                                         v[e + 3] = o.w + sw * __uint_as_float(raw[e + 3]);
                                     }
-                                    if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
+                                    if (in_range && !(p.debug & 128)) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
                                 } else {
 #pragma unroll
                                     for (int e = 0; e < 32; e += 4) {
@@ -707,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         *q = o;
                                     }
                                 }
-                            } else {
+                            } else if (!(p.debug & 256)) {
                                 // L2 workspace slot
                                 float* pt = whole ? partial_tile<BN>(p, slot, home, true)
                                                   : partial_tile<BN>(p, slot, ij, false);
@@ -718,16 +722,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                                     for (int e = 0; e < 32; ++e) v[e] = sw * __uint_as_float(raw[e]);
                                     if (!first) {
-                                        float4 o[8];
+                                        // two batches of 4 loads (register budget: the
+                                        // register partial, H and v are live here)
 #pragma unroll
-                                        for (int q = 0; q < 8; ++q) o[q] = ld_cg_f4(pt + partial_off(row, c4 + q));
+                                        for (int b = 0; b < 8; b += 4) {
+                                            float4 o[4];
 #pragma unroll
-                                        for (int q = 0; q < 8; ++q) {
-                                            v[4 * q] += o[q].x; v[4 * q + 1] += o[q].y;
-                                            v[4 * q + 2] += o[q].z; v[4 * q + 3] += o[q].w;
+                                            for (int q = 0; q < 4; ++q) o[q] = ld_cg_f4(pt + partial_off(row, c4 + b + q));
+#pragma unroll
+                                            for (int q = 0; q < 4; ++q) {
+                                                v[4 * (b + q)] += o[q].x; v[4 * (b + q) + 1] += o[q].y;
+                                                v[4 * (b + q) + 2] += o[q].z; v[4 * (b + q) + 3] += o[q].w;
+                                            }
                                         }
                                     }
-                                    if (in_range) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
+                                    if (in_range && !(p.debug & 128)) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
                                     if (!first && p.discard) {
                                         __syncwarp();      // the 8 lanes sharing a line have read it
                                         if ((row & 7) == 0) discard_lines(pt, row, c4, 8);
