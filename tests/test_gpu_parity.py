@@ -350,3 +350,23 @@ def test_fake_multi_gpu_block_rows():
         parts.append(plan.gemm(A[r0:r1].cuda(), B.cuda()).cpu())
     C = torch.cat(parts).numpy()
     assert np.array_equal(C, O.gemm_i64(A.to(torch.int64).numpy(), B.to(torch.int64).numpy()))
+
+
+@pytest.mark.parametrize("env", [
+    {},                                                   # registers + shared memory (col half 0) + L2
+    {"LCMA_QFULL": "1"},                                  # shared-memory home over both column halves
+    {"LCMA_REG_PARTIAL": "0"},                            # no register home
+    {"LCMA_SMEM_PARTIAL": "0"},                           # no shared-memory home
+    {"LCMA_REG_PARTIAL": "0", "LCMA_SMEM_PARTIAL": "0"},  # every partial in L2 (r01e layout)
+    {"LCMA_SERPENTINE": "1"},                             # odd rounds in reverse product order
+    {"LCMA_ORDER": "0"},                                  # natural product order, one L2 slot per C_ij
+])
+@pytest.mark.parametrize("algo,shape,ctas", [("strassen", (1536, 2304, 512), 0), ("strassen", (1536, 2304, 512), 10),
+                                             ("laderman", (1000, 808, 520), 0), ("strassen2", (1024, 1024, 512), 0)])
+def test_partial_homes_exact(monkeypatch, env, algo, shape, ctas):
+    # fused Combine H keeps live C_ij partials in epilogue registers, shared
+    # memory or L2 slots (launch-time knobs); every placement must give the
+    # exact result, whole groups and split tail groups alike
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _exact_case(*shape, algo, variant="fused_h", num_ctas=ctas)

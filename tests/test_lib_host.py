@@ -188,3 +188,22 @@ def test_partial_slots_product_order():
         assert 1 <= s <= mn
     assert L.Plan(4096, 4096, 4096, algo="classical").info["partial_slots"] == 0
     assert L.Plan(4096, 4096, 4096, algo="strassen", variant="unfused").info["partial_slots"] == 0
+
+
+def test_l2_partial_transfers_per_group():
+    # fused Combine H: the two most-updated partial slots live on chip
+    # (registers; shared memory for column half 0), the rest move through L2.
+    # Strassen: 2 live slots -> only half of the shared-memory slot's 6 tile
+    # transfers (its C_ij uses) go to L2.
+    import ctypes
+    f = L.lib().lcma_debug_l2_partial_tiles
+    f.restype, f.argtypes = ctypes.c_double, [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
+    live = ctypes.c_int32()
+    assert f(1, ctypes.byref(live)) == 3.0 and live.value == 2      # Strassen
+    assert f(0, ctypes.byref(live)) == 0.0 and live.value == 0      # classical
+    for sid in (2, 3):                                              # Strassen^2 (flat), Laderman
+        m, k, n, R, U, V, W = L.scheme_get(sid)
+        t = f(sid, ctypes.byref(live))
+        assert 2 < live.value <= m * n
+        # never more than every nonzero W entry moving through L2
+        assert 0 < t <= int(np.count_nonzero(W))
