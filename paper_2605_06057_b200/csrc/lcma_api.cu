@@ -603,12 +603,12 @@ lcma_status check_launch(const char* what) {
     return LCMA_OK;
 }
 
-template <int CG, int BN, int QF = 0>
+template <int CG, int BN, int QF = 0, bool REGH = false>
 lcma_status ensure_smem_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        err = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    Cfg<CG, BN, QF>::kSmemBytes);
     });
     if (err != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
@@ -727,8 +727,14 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     int qf = 0;
     if (const char* v = std::getenv("LCMA_QFULL"))
         qf = (!classical && !H && p->cg == 2 && p->bn == 256 && S.m * S.n > 1 && std::atoi(v) != 0) ? 1 : 0;
+    // REGH: the instantiation with a register partial home (fused Combine H of
+    // an LCMA scheme on 256-column pair tiles); classical / unfused GEMMs use
+    // the one without (no 128 live registers reserved in the epilogue)
+    const bool regh = !classical && !H && p->cg == 2 && p->bn == 256;
     lcma_status rs = p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
-                                                : (qf ? ensure_smem_attr<2, 256, 1>() : ensure_smem_attr<2, 256>()))
+                                                : (qf ? ensure_smem_attr<2, 256, 1, true>()
+                                                      : regh ? ensure_smem_attr<2, 256, 0, true>()
+                                                             : ensure_smem_attr<2, 256>()))
                                 : (p->bn == 128 ? ensure_smem_attr<1, 128>() : ensure_smem_attr<1, 256>());
     if (rs != LCMA_OK) return rs;
     const lcma_dtype dt = p->d.dtype;
@@ -820,7 +826,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         // slot -> home
         const int ns = po.nslot;
         const std::vector<int>& by_use = po.by_use;
-        const bool use_reg = !H && !(std::getenv("LCMA_REG_PARTIAL") && std::atoi(std::getenv("LCMA_REG_PARTIAL")) == 0);
+        const bool use_reg = regh && !(std::getenv("LCMA_REG_PARTIAL") && std::atoi(std::getenv("LCMA_REG_PARTIAL")) == 0);
         const bool use_smem = !H && !(std::getenv("LCMA_SMEM_PARTIAL") && std::atoi(std::getenv("LCMA_SMEM_PARTIAL")) == 0);
         std::vector<int> slot_home(ns, 0);
         int nl2 = 0, k0 = 0;
@@ -886,7 +892,10 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     cudaError_t e;
     if (p->cg == 2 && p->bn == 256 && qf) {
         cfg.dynamicSmemBytes = Cfg<2, 256, 1>::kSmemBytes;
-        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 1>, ta, tb, g);
+        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 1, true>, ta, tb, g);
+    } else if (p->cg == 2 && p->bn == 256 && regh) {
+        cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
+        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256) {
         cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256>, ta, tb, g);

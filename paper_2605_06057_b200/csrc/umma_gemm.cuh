@@ -348,7 +348,7 @@ __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, unsig
 }
 
 // ------------------------------------------------------------ the kernel
-template <int CG, int BN, int QF = 0>
+template <int CG, int BN, int QF = 0, bool REGH = false>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
@@ -587,7 +587,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             CG == 2 ? ptx::mapa_shared(ptx::smem_u32(&tempty_bar[0]), 0) : 0u;
         int acc = 0;
         uint32_t acc_phase = 0;
-        float preg[BN / 2];       // HOME_REG partial: (row, this thread's column half)
+        // HOME_REG partial: (row, this thread's column half); one dummy
+        // register when the instantiation has no register home (REGH false:
+        // classical and unfused GEMMs keep the register budget)
+        constexpr int kPregCols = REGH ? BN / 2 : 1;
+        float preg[kPregCols];
         UnitIter it(p, w);
         Unit u;
         while (it.next(u)) {
@@ -664,9 +668,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
                             const long long ccol = (long long)j * p.Nb + (long long)z * BN + col_base + ch * 32;
                             const bool in_range = brow < p.Mb && ccol < (long long)(j + 1) * p.Nb;
-                            if (whole && home == HOME_REG) {
+                            if (!REGH && home == HOME_REG) home = 0;   // (the host never assigns it here)
+                            if (REGH && whole && home == HOME_REG) {
                                 if (p.debug & 1024) continue;
-                                float* pr = &preg[ch * 32];
+                                float* pr = &preg[(ch * 32) % kPregCols];
                                 if (final_here) {
                                     // the partial dies here: finish C in place (no extra
                                     // 32-register buffer; a first contribution of this
