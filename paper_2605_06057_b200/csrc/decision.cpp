@@ -92,7 +92,20 @@ double estimate_time_b200(const Scheme& s, double M, double N, double K, const P
     t += (M * K + R * Mb * Kb) / hw.beta_combine;                       // Combine A
     if (!b_static) t += (K * N + R * Kb * Nb) / hw.beta_combine;        // Combine B
     const double t_mma = 2.0 * R * Mb * Nb * Kb / hw.flops_mul;         // R sub-GEMMs
-    if (fused) {
+    if (fused && s.base_id >= 0) {
+        // depth 2 runs two-level (LCMA_VARIANT_TWO_LEVEL): per outer product q
+        // one fused-Combine-H GEMM of the base scheme writes the outer H_q in
+        // fp32, then the outer Combine H reads them back and writes C
+        const Scheme& b = *scheme_get(s.base_id);
+        const double l2_tiles = scheme_product_order(b.id).l2_tiles;
+        const double Kb_in = Kb;                                         // inner k-extent per product
+        const double partial = l2_tiles * 128.0 * tileN * 4.0;
+        const double operand = b.R * (Kb_in / BK) * (128.0 * 128.0 + 128.0 * 128.0);
+        const double rho = partial / operand;
+        t += t_mma * (1.0 + hw.epi_overhead + hw.alpha_partial * rho * rho);
+        const double hq = (double)b.R * std::ceil(M / b.m) * std::ceil(N / b.n) * 4.0;   // outer H_q bytes
+        t += (2.0 * hq + M * N * elem_bytes) / (hw.beta * elem_bytes);
+    } else if (fused) {
         const double l2_tiles = scheme_product_order(s.id).l2_tiles;   // partial tile transfers per CTA and group
         const double partial = l2_tiles * 128.0 * tileN * 4.0;          // fp32 partial bytes per CTA and group
         const double operand = R * (Kb / BK) * (128.0 * 128.0 + 128.0 * 128.0);   // A + B half per CTA and group
