@@ -207,3 +207,19 @@ def test_l2_partial_transfers_per_group():
         assert 2 < live.value <= m * n
         # never more than every nonzero W entry moving through L2
         assert 0 < t <= int(np.count_nonzero(W))
+
+
+def test_b200_model_two_level_and_partial_terms():
+    # B200 decision model (decision_model=0): depth 2 executes two-level, so
+    # its estimate carries the outer H_q fp32 round trip; fewer L2 partial
+    # transfers (Strassen) must not cost more than many (Laderman) per flop
+    M, N, K = 8192, 14336, 4096
+    t = {a: L.Plan(M, N, K, algo=a).info["t_pred_choice"] for a in ("classical", "strassen", "strassen2", "laderman")}
+    hq = 2 * 7 * (M // 2) * (N // 2) * 4 / 6.55e12          # outer H_q written + read, fp32, at HBM speed
+    assert t["strassen2"] > t["strassen"] + 0.5 * hq
+    # Laderman: 33 L2 partial transfers per group vs Strassen's 3
+    assert t["laderman"] > t["strassen"]
+    # tf32 grid corner of cfg3: AUTO picks depth-1 Strassen (measured best, r01f/r01g)
+    assert L.Plan(16384, 14336, 14336, dtype=L.TF32, algo="auto").info["scheme"].startswith("strassen-2x2x2")
+    # 16-bit cfg2: classical (measured best)
+    assert L.Plan(M, N, K, dtype=L.BF16, algo="auto").info["scheme"] == "classical"
