@@ -415,8 +415,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             unsigned long long w_empty = 0;
             unsigned long long* st_empty = p.stats ? &w_empty : nullptr;
-            const uint64_t opol = p.operand_hint == 2 ? ptx::policy_evict_last() : ptx::policy_evict_first();
-            const bool ohint = p.operand_hint != 0;
+            // L2 policies of the operand loads: 1 both evict_first, 2 both
+            // evict_last, 3 A evict_last / B evict_first (A panels are reused by
+            // the rounds of a band, B panels stream), 4 the reverse
+            const int oh = p.operand_hint;
+            const uint64_t opol = oh == 2 || oh == 3 ? ptx::policy_evict_last() : ptx::policy_evict_first();
+            const uint64_t opol_b = oh == 2 || oh == 4 ? ptx::policy_evict_last() : ptx::policy_evict_first();
+            const bool ohint = oh != 0;
             UnitIter it(p, w);
             Unit u;
             while (it.next(u)) {
@@ -474,14 +479,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                      ((r + e) % p.R) * p.b_rows_per_r + b_col0, ohint, opol);
                             if (!skip_a) ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
                             if (!p.b_mn_major) {
-                                ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol);
+                                ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol_b);
                             } else if (p.b_3d) {
                                 ptx::tma_load_3d_cg2(sb, &tmap_b, lbar, 0, r * p.b_rows_per_r + kcol,
                                                      b_col0 / p.BK);
                             } else {
                                 for (int c = 0; c < n_chunks; ++c)
                                     ptx::tma_load_2d_cg2(sb + c * b_bytes_chunk, &tmap_b, lbar,
-                                                         b_col0 + c * p.BK, r * p.b_rows_per_r + kcol, ohint, opol);
+                                                         b_col0 + c * p.BK, r * p.b_rows_per_r + kcol, ohint, opol_b);
                             }
                         }
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
