@@ -58,12 +58,12 @@ int max_active_pairs() {
         int dev = 0;
         if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
         if (cudaFuncSetAttribute(umma_gemm_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg<2, 256>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return; }
+                                 Cfg<2, 256, 0, true>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return; }
         cudaLaunchConfig_t cfg;
         std::memset(&cfg, 0, sizeof(cfg));
         cfg.gridDim = dim3(2);
         cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
+        cfg.dynamicSmemBytes = Cfg<2, 256, 0, true>::kSmemBytes;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
@@ -609,7 +609,7 @@ lcma_status ensure_smem_attr() {
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
         err = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   Cfg<CG, BN, QF>::kSmemBytes);
+                                   Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value>::kSmemBytes);
     });
     if (err != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
     return LCMA_OK;
@@ -897,7 +897,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256) {
-        cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
+        cfg.dynamicSmemBytes = Cfg<2, 256, 0, true>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256>, ta, tb, g);
     } else if (p->cg == 2) {
         cfg.dynamicSmemBytes = Cfg<2, 128>::kSmemBytes;
@@ -1070,14 +1070,14 @@ extern "C" double lcma_debug_l2_partial_tiles(int32_t scheme_id, int32_t* live) 
 
 extern "C" int lcma_debug_max_clusters(int cluster_size) {
     if (cudaFuncSetAttribute(umma_gemm_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg<2, 256>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return -1; }
+                             Cfg<2, 256, 0, true>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return -1; }
     if (cluster_size > 8)
         cudaFuncSetAttribute(umma_gemm_kernel<2, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(cluster_size);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
+    cfg.dynamicSmemBytes = Cfg<2, 256, 0, true>::kSmemBytes;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cluster_size;

@@ -48,7 +48,12 @@ constexpr int kMaxMN = 32;
 // QF = 1: the shared-memory C_ij partial covers the whole 128 x BN slab of
 // the CTA (128 KB for BN = 256, leaving room for 3 operand stages); QF = 0:
 // only column half 0 (64 KB, 4 stages), half 1 of that partial goes to L2.
-template <int CG, int BN = kBN, int QF = 0>
+#ifndef LCMA_MAX_STAGES_NP
+#define LCMA_MAX_STAGES_NP 5      // ring depth of the instantiation without a partial area (classical)
+#endif
+// NP: no shared-memory partial area (the classical / unfused instantiation of
+// the 256-column pair kernel), so the ring may use that space.
+template <int CG, int BN = kBN, int QF = 0, bool NP = false>
 struct Cfg {
     static constexpr int kTileM = kBM * CG;                  // rows per group tile
     static constexpr int kBNc = BN / CG;                     // B columns staged per CTA
@@ -57,13 +62,20 @@ struct Cfg {
     static constexpr int kStageBytes = kABytes + kBBytes;
     // one C_ij partial kept in shared memory (fused Combine H, whole groups):
     // 128 rows x BN (QF) or BN/2 (column half 0) fp32
-    static constexpr int kPartialSmem = kBM * (QF ? BN : BN / 2) * 4;
+    static constexpr int kPartialSmem = NP ? 0 : kBM * (QF ? BN : BN / 2) * 4;
+    static constexpr int kMaxStages = NP ? LCMA_MAX_STAGES_NP : LCMA_MAX_STAGES;
     // as many stages as fit in 227 KB (minus the partial, alignment slack and
     // barriers), <= LCMA_MAX_STAGES
     static constexpr int kFree = 232448 - 1024 - 256 - kPartialSmem;
-    static constexpr int kStages = (kFree / kStageBytes) > LCMA_MAX_STAGES ? LCMA_MAX_STAGES
-                                                                           : (kFree / kStageBytes);
+    static constexpr int kStages = (kFree / kStageBytes) > kMaxStages ? kMaxStages : (kFree / kStageBytes);
     static constexpr int kSmemBytes = kStages * kStageBytes + kPartialSmem + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// The 256-column pair kernel without a register home is only launched for
+// classical / unfused GEMMs (no partial homes): no shared-memory partial area.
+template <int CG, int BN, int QF, bool REGH>
+struct KernelNP {
+    static constexpr bool value = CG == 2 && BN == 256 && QF == 0 && !REGH;
 };
 
 enum EpiMode : int { EPI_FUSED = 0, EPI_STORE_H = 1 };
@@ -353,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ GemmParams p) {
-    using C_ = Cfg<CG, BN, QF>;
+    using C_ = Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value>;
     constexpr int kStages = C_::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
