@@ -10,11 +10,18 @@
 //         its 128 rows of A and its 128 columns of B, so per-SM shared-memory
 //         and L2 operand traffic per MMA flop are halved for B.
 //
-// Roles per CTA (384 threads):
+// Roles per CTA (384 threads; setmaxnreg moves registers from warpgroup 0,
+// 40 per thread, to the two epilogue warpgroups, 232 per thread):
 //   warp 0      TMA producer: At_r[x, y] and Bt_r[y, z] tiles -> smem ring
 //   warp 1      MMA issuer (leader CTA only): one thread issues tcgen05.mma
 //   warp 2      TMEM allocator (512 columns = 2 fp32 accumulators of 256)
-//   warps 4-11  epilogue: TMEM -> registers -> (Combine H) -> global
+//   warps 4-11  epilogue: TMEM -> registers -> (Combine H) -> global; each
+//               thread owns one row x 128 columns of the CTA's 128 x 256 slab
+//
+// Fused Combine H keeps the live C_ij partials of a whole group on chip where
+// it can (GemmParams::home): the most-updated slot in the epilogue threads'
+// registers (REGH instantiation), the next in shared memory (column half 0)
+// with column half 1 in an L2 workspace tile, further slots in L2 tiles.
 //
 // Work decomposition (Group-Parallel Optimization): a *group* is
 // the set {H_r[x,z]}_{r=1..R} of one output tile position (x,z); the CTA (pair)
