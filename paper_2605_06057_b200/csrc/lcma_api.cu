@@ -237,8 +237,20 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         if (variant == LCMA_VARIANT_AUTO)
             variant = p->sch.base_id >= 0 ? LCMA_VARIANT_TWO_LEVEL : LCMA_VARIANT_FUSED_H;
         if (variant == LCMA_VARIANT_PRODUCER) {
-            delete p;
-            return fail(LCMA_ERR_NOT_SUPPORTED, "producer-fused variant not built (DESIGN.md section 7)");
+            // Combine A in the GEMM producer path (two A source blocks at most
+            // per product, summed in shared memory by warps 2-3): measured
+            // variant, not the default
+            bool ok = p->sch.R <= kMaxR;
+            for (int r = 0; r < p->sch.R && ok; ++r) {
+                int nz = 0;
+                for (int a = 0; a < p->sch.m; ++a)
+                    for (int b = 0; b < p->sch.k; ++b) nz += p->sch.u(r, a, b) != 0;
+                ok = nz >= 1 && nz <= 2;
+            }
+            if (!ok) {
+                delete p;
+                return fail(LCMA_ERR_NOT_SUPPORTED, "producer-fused variant: at most two A blocks per product");
+            }
         }
         if (variant == LCMA_VARIANT_TWO_LEVEL && p->sch.base_id < 0) {
             delete p;
@@ -298,6 +310,13 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         }
         p->G = p->nX * p->nZ;
         make_schedule(p, (d.schedule == 2 || d.schedule == 3) ? d.schedule : 1);
+        if (variant == LCMA_VARIANT_PRODUCER &&
+            (p->cg != 2 || p->bn != 256 || d.M != (int64_t)S.m * p->Mb || d.K != (int64_t)S.k * p->Kb)) {
+            delete p;
+            return fail(LCMA_ERR_NOT_SUPPORTED,
+                        "producer-fused variant: needs 256-column CTA-pair tiles and M, K that the m x k "
+                        "block grid tiles exactly (the source blocks are read in place)");
+        }
     }
 
     // ---- two-level: the inner (base-scheme) fused GEMM over the composed
@@ -332,7 +351,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     p->off_P = p->off_flags = p->off_At = p->off_Bt = p->off_H = 0;
     const int mn = S.m * S.n;
     if (!classical) {
-        if (d.dtype != LCMA_FP32 && variant == LCMA_VARIANT_FUSED_H) {
+        if (d.dtype != LCMA_FP32 && (variant == LCMA_VARIANT_FUSED_H || variant == LCMA_VARIANT_PRODUCER)) {
             p->off_P = off;
             off = align256(off + (size_t)3 * p->ctas * mn * kBM * p->bn * sizeof(float));
             p->off_flags = off;
@@ -387,7 +406,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     I.workspace_bytes = p->ws_bytes;
     I.btilde_bytes = p->bt_bytes;
     I.partial_slots = 0;
-    if (!classical && d.dtype != LCMA_FP32 && variant == LCMA_VARIANT_FUSED_H) {
+    if (!classical && d.dtype != LCMA_FP32 && (variant == LCMA_VARIANT_FUSED_H || variant == LCMA_VARIANT_PRODUCER)) {
         const bool use_order = !std::getenv("LCMA_ORDER") || std::atoi(std::getenv("LCMA_ORDER")) != 0;
         I.partial_slots = use_order ? scheme_product_order(p->scheme_id).nslot : S.m * S.n;
     }
@@ -603,13 +622,13 @@ lcma_status check_launch(const char* what) {
     return LCMA_OK;
 }
 
-template <int CG, int BN, int QF = 0, bool REGH = false>
+template <int CG, int BN, int QF = 0, bool REGH = false, bool PF = false>
 lcma_status ensure_smem_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value>::kSmemBytes);
+        err = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF>::kSmemBytes);
     });
     if (err != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
     return LCMA_OK;
@@ -718,7 +737,7 @@ lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cuda
 // tcgen05 GEMM: classical (R == 1 over A, B) or the LCMA GEMM stage over the
 // materialised At / Bt with the fused Combine H (or H store) epilogue.
 lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, void* C, float* P,
-                        int* flags, float* H, cudaStream_t st) {
+                        int* flags, float* H, cudaStream_t st, bool pf = false) {
     const Scheme& S = p->sch;
     const bool classical = p->scheme_id == SCHEME_CLASSICAL;
     // QF: the shared-memory partial home covers both column halves (3 operand
@@ -731,7 +750,9 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     // an LCMA scheme on 256-column pair tiles); classical / unfused GEMMs use
     // the one without (no 128 live registers reserved in the epilogue)
     const bool regh = !classical && !H && p->cg == 2 && p->bn == 256;
-    lcma_status rs = p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
+    if (pf) qf = 0;
+    lcma_status rs = pf ? ensure_smem_attr<2, 256, 0, true, true>()
+                   : p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
                                                 : (qf ? ensure_smem_attr<2, 256, 1, true>()
                                                       : regh ? ensure_smem_attr<2, 256, 0, true>()
                                                              : ensure_smem_attr<2, 256>()))
@@ -740,9 +761,9 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     const lcma_dtype dt = p->d.dtype;
     const int epr = 128 / p->e;           // elements per 128-byte row
     CUtensorMap ta, tb;
-    // A operand: K-major rows
-    const uint64_t a_cols = classical ? p->d.K : p->Kb;
-    const uint64_t a_rows = classical ? p->d.M : (uint64_t)S.R * p->Mb;
+    // A operand: K-major rows (PF: the raw A, its blocks are combined in the kernel)
+    const uint64_t a_cols = (classical || pf) ? p->d.K : p->Kb;
+    const uint64_t a_rows = (classical || pf) ? p->d.M : (uint64_t)S.R * p->Mb;
     rs = make_map(&ta, Aop, dt, a_cols, a_rows, epr, kBM);
     if (rs != LCMA_OK) return rs;
     const bool b_mn = p->d.b_layout == 0;
@@ -827,7 +848,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         const int ns = po.nslot;
         const std::vector<int>& by_use = po.by_use;
         const bool use_reg = regh && !(std::getenv("LCMA_REG_PARTIAL") && std::atoi(std::getenv("LCMA_REG_PARTIAL")) == 0);
-        const bool use_smem = !H && !(std::getenv("LCMA_SMEM_PARTIAL") && std::atoi(std::getenv("LCMA_SMEM_PARTIAL")) == 0);
+        const bool use_smem = !H && !pf && !(std::getenv("LCMA_SMEM_PARTIAL") && std::atoi(std::getenv("LCMA_SMEM_PARTIAL")) == 0);
         std::vector<int> slot_home(ns, 0);
         int nl2 = 0, k0 = 0;
         if (use_reg && k0 < ns) slot_home[by_use[k0++]] = HOME_REG;
@@ -890,7 +911,24 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     cfg.attrs = attr;
     cfg.numAttrs = na;
     cudaError_t e;
-    if (p->cg == 2 && p->bn == 256 && qf) {
+    if (pf) {
+        g.kgrid = S.k;
+        g.pf_Kb = (int)p->Kb;
+        for (int r = 0; r < S.R; ++r) {
+            g.pf_blk0[r] = g.pf_blk1[r] = -1;
+            g.pf_s0[r] = g.pf_s1[r] = 0;
+            for (int a = 0; a < S.m; ++a)
+                for (int b = 0; b < S.k; ++b) {
+                    const int v = S.u(r, a, b);
+                    if (!v) continue;
+                    if (g.pf_blk0[r] < 0) { g.pf_blk0[r] = (int8_t)(a * S.k + b); g.pf_s0[r] = (int8_t)v; }
+                    else { g.pf_blk1[r] = (int8_t)(a * S.k + b); g.pf_s1[r] = (int8_t)v; }
+                }
+        }
+        g.debug &= ~(16 | 32 | 64);   // stale-operand / extra-load diagnostics do not apply
+        cfg.dynamicSmemBytes = Cfg<2, 256, 0, false, true>::kSmemBytes;
+        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, true>, ta, tb, g);
+    } else if (p->cg == 2 && p->bn == 256 && qf) {
         cfg.dynamicSmemBytes = Cfg<2, 256, 1>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 1, true>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256 && regh) {
@@ -970,8 +1008,11 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
     }
     void* At = w + p->off_At;
     const void* Bt = Bt_user;
-    lcma_status rs = launch_combine(p, A, At, false, st);          // Combine A (Eq. 3)
-    if (rs != LCMA_OK) return rs;
+    lcma_status rs = LCMA_OK;
+    if (p->variant != LCMA_VARIANT_PRODUCER) {
+        rs = launch_combine(p, A, At, false, st);                  // Combine A (Eq. 3)
+        if (rs != LCMA_OK) return rs;
+    }
     if (!Bt) {
         rs = launch_combine(p, B, w + p->off_Bt, true, st);        // Combine B (Eq. 4)
         if (rs != LCMA_OK) return rs;
@@ -1014,6 +1055,9 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
         if (rs != LCMA_OK) return rs;
         return launch_combine_h(p, H, C, st);
     }
+    if (p->variant == LCMA_VARIANT_PRODUCER)   // Combine A (Eq. 3) inside the GEMM's producer path
+        return launch_umma(p, A, Bt, C, reinterpret_cast<float*>(w + p->off_P),
+                           reinterpret_cast<int*>(w + p->off_flags), nullptr, st, true);
     return launch_umma(p, At, Bt, C, reinterpret_cast<float*>(w + p->off_P),
                        reinterpret_cast<int*>(w + p->off_flags), nullptr, st);
 }

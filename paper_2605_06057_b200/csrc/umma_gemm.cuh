@@ -60,16 +60,18 @@ constexpr int kMaxMN = 32;
 #endif
 // NP: no shared-memory partial area (the classical / unfused instantiation of
 // the 256-column pair kernel), so the ring may use that space.
-template <int CG, int BN = kBN, int QF = 0, bool NP = false>
+// PF: producer-fused Combine A (variant 3): a staging slot per stage for the
+// second A source block, no shared-memory partial area.
+template <int CG, int BN = kBN, int QF = 0, bool NP = false, bool PF = false>
 struct Cfg {
     static constexpr int kTileM = kBM * CG;                  // rows per group tile
     static constexpr int kBNc = BN / CG;                     // B columns staged per CTA
     static constexpr int kABytes = kBM * 128;                // 128 rows x 128 bytes
     static constexpr int kBBytes = kBNc * 128;               // kBNc x 128 B (K-major) or chunks (MN-major)
-    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStageBytes = kABytes + kBBytes + (PF ? kABytes : 0);   // PF: + A staging
     // one C_ij partial kept in shared memory (fused Combine H, whole groups):
     // 128 rows x BN (QF) or BN/2 (column half 0) fp32
-    static constexpr int kPartialSmem = NP ? 0 : kBM * (QF ? BN : BN / 2) * 4;
+    static constexpr int kPartialSmem = (NP || PF) ? 0 : kBM * (QF ? BN : BN / 2) * 4;
     static constexpr int kMaxStages = NP ? LCMA_MAX_STAGES_NP : LCMA_MAX_STAGES;
     // as many stages as fit in 227 KB (minus the partial, alignment slack and
     // barriers), <= LCMA_MAX_STAGES
@@ -133,6 +135,11 @@ struct GemmParams {
     int pace_ns;           // >0: sleep between C_ij updates (spreads epilogue traffic)
     int nslot;             // partial tiles live at once for whole groups (<= m*n)
     int serpentine;        // odd lockstep rounds process their products in reverse order
+    // producer-fused Combine A (PF kernel): At_r = s0 * A_blk0 + s1 * A_blk1,
+    // blocks i*k + l of the raw A map (blk1 = -1: one block)
+    int kgrid;             // scheme k
+    int pf_Kb;             // block extent along K (columns of a source block)
+    int8_t pf_blk0[kMaxR], pf_blk1[kMaxR], pf_s0[kMaxR], pf_s1[kMaxR];
     int qslot;             // QF = 0: L2 slot of the column half 1 of the HOME_SMEM partial
     int8_t home[kMaxMN];   // whole groups: C_ij partial home (HOME_REG, HOME_SMEM, or L2 slot >= 0)
     int8_t rperm[kMaxR];   // product processing order inside a group (t -> r)
@@ -367,12 +374,12 @@ __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, unsig
 }
 
 // ------------------------------------------------------------ the kernel
-template <int CG, int BN, int QF = 0, bool REGH = false>
+template <int CG, int BN, int QF = 0, bool REGH = false, bool PF = false>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ GemmParams p) {
-    using C_ = Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value>;
+    using C_ = Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF>;
     constexpr int kStages = C_::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -383,6 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull_bar = empty_bar + kStages;   // [2]
     uint64_t* tempty_bar = tfull_bar + 2;        // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* ld_bar = tempty_bar + 4;           // PF: [kStages] own A tiles landed (local)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -399,8 +407,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&tmap_a);
         ptx::tma_prefetch_desc(&tmap_b);
         for (int s = 0; s < kStages; ++s) {
-            ptx::mbar_init(&full_bar[s], 1);        // the leader's expect_tx arrival
+            // the leader's expect_tx arrival (+ PF: one arrival per combine warp
+            // of both CTAs once the combined A tile is in place)
+            ptx::mbar_init(&full_bar[s], PF ? 1 + 2 * CG : 1);
             ptx::mbar_init(&empty_bar[s], 1);       // one commit per stage
+            if constexpr (PF) ptx::mbar_init(&ld_bar[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull_bar[a], 1);
@@ -485,10 +496,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // diagnostics (debug bit 6): A tile loaded only on even k-blocks,
                             // i.e. the L2 operand traffic of an A-multicast cluster of 2 pairs
                             const bool skip_a = (p.debug & 64) && (kb & 1);
-                            if (leader)
-                                ptx::mbar_arrive_expect_tx(&full_bar[stage],
-                                                           (C_::kStageBytes - (skip_a ? C_::kABytes : 0) +
-                                                            ea * C_::kABytes + eb * C_::kBBytes) * CG);
+                            if (leader) {
+                                if constexpr (PF) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kBBytes * CG);
+                                else
+                                    ptx::mbar_arrive_expect_tx(&full_bar[stage],
+                                                               (C_::kStageBytes - (skip_a ? C_::kABytes : 0) +
+                                                                ea * C_::kABytes + eb * C_::kBBytes) * CG);
+                            }
                             for (int e = 1; e <= ea; ++e)
                                 ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol,
                                                      ((r + e) % p.R) * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM,
@@ -496,7 +510,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int e = 1; e <= eb && !p.b_mn_major; ++e)
                                 ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol,
                                                      ((r + e) % p.R) * p.b_rows_per_r + b_col0, ohint, opol);
-                            if (!skip_a) ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
+                            if constexpr (PF) {
+                                // Combine A in the producer path: the (one or two) nonzero
+                                // A blocks land in this CTA's A slot and staging slot on
+                                // the local ld_bar; the combine warps sum them
+                                const int b0 = p.pf_blk0[r], b1 = p.pf_blk1[r];
+                                const int xr = x * C_::kTileM + (int)rank * kBM;
+                                ptx::mbar_arrive_expect_tx(&ld_bar[stage], (b1 >= 0 ? 2 : 1) * C_::kABytes);
+                                ptx::tma_load_2d(sa, &tmap_a, &ld_bar[stage], (b0 % p.kgrid) * p.pf_Kb + kcol,
+                                                 (b0 / p.kgrid) * (int)p.Mb + xr);
+                                if (b1 >= 0)
+                                    ptx::tma_load_2d(sa + C_::kABytes + C_::kBBytes, &tmap_a, &ld_bar[stage],
+                                                     (b1 % p.kgrid) * p.pf_Kb + kcol, (b1 / p.kgrid) * (int)p.Mb + xr);
+                            } else if (!skip_a) {
+                                ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
+                            }
                             if (!p.b_mn_major) {
                                 ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol_b);
                             } else if (p.b_3d) {
@@ -596,6 +624,60 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp < kEpiWarp0) {
         ptx::setmaxnreg_dec<40>();   // allocator / idle warps
+        if constexpr (PF && CG == 2) {
+            // ================================ Combine A (PF): warps 2-3 of both CTAs
+            // At_r tile = s0 * A_blk0 + s1 * A_blk1 in fp32, one RN rounding to
+            // the 16-bit type, written over the A slot (both source tiles carry
+            // the same 128B swizzle, so the sum is element-wise on raw bytes)
+            const int ct = (warp - 2) * 32 + lane;            // 0..63
+            const uint32_t full_leader0 = ptx::mapa_shared(ptx::smem_u32(&full_bar[0]), 0);
+            const bool bf16 = ((p.idesc >> 7) & 7u) == 1u;   // kind::f16 a_format: 1 = bf16, 0 = fp16
+            int stage = 0;
+            uint32_t phase = 0;
+            UnitIter it(p, w);
+            Unit u;
+            while (it.next(u)) {
+                for (int t = u.r0; t < u.r1; ++t) {
+                    const int r = product_at(p, u, t);
+                    const float s0 = (float)p.pf_s0[r], s1 = (float)p.pf_s1[r];
+                    const bool two = p.pf_blk1[r] >= 0;
+                    for (int kb = 0; kb < p.nK; ++kb) {
+                        ptx::mbar_wait(&ld_bar[stage], phase);
+                        if (two || s0 < 0.f) {
+                            uint8_t* sa = smem + stage * C_::kStageBytes;
+                            const uint8_t* sx = sa + C_::kABytes + C_::kBBytes;
+                            for (int q = ct; q < C_::kABytes / 16; q += 64) {
+                                uint4 a = *reinterpret_cast<const uint4*>(sa + q * 16);
+                                uint4 b = two ? *reinterpret_cast<const uint4*>(sx + q * 16) : make_uint4(0, 0, 0, 0);
+                                uint32_t* pa = reinterpret_cast<uint32_t*>(&a);
+                                const uint32_t* pb = reinterpret_cast<const uint32_t*>(&b);
+#pragma unroll
+                                for (int h = 0; h < 4; ++h) {
+                                    float2 fa, fb;
+                                    if (bf16) {
+                                        fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pa[h]));
+                                        fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pb[h]));
+                                        __nv_bfloat162 o = __floats2bfloat162_rn(s0 * fa.x + s1 * fb.x, s0 * fa.y + s1 * fb.y);
+                                        pa[h] = *reinterpret_cast<uint32_t*>(&o);
+                                    } else {
+                                        fa = __half22float2(*reinterpret_cast<const __half2*>(&pa[h]));
+                                        fb = __half22float2(*reinterpret_cast<const __half2*>(&pb[h]));
+                                        __half2 o = __floats2half2_rn(s0 * fa.x + s1 * fb.x, s0 * fa.y + s1 * fb.y);
+                                        pa[h] = *reinterpret_cast<uint32_t*>(&o);
+                                    }
+                                }
+                                *reinterpret_cast<uint4*>(sa + q * 16) = a;
+                            }
+                            // generic-proxy writes -> visible to the tensor core (async proxy)
+                            ptx::fence_proxy_async_smem();
+                        }
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive_cluster(full_leader0 + stage * 8);
+                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
     } else {
         // ================================ epilogue (both CTAs: own 128 rows)
         ptx::setmaxnreg_inc<232>();

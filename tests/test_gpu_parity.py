@@ -370,3 +370,20 @@ def test_partial_homes_exact(monkeypatch, env, algo, shape, ctas):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _exact_case(*shape, algo, variant="fused_h", num_ctas=ctas)
+
+
+@pytest.mark.parametrize("b_layout", [0, 1])
+@pytest.mark.parametrize("shape,dtype,ctas", [((512, 512, 512), 0, 0), ((1024, 1560, 768), 0, 0),
+                                              ((1536, 2304, 512), 0, 10), ((1024, 1032, 768), 1, 0)])
+def test_producer_fused_combine_a_exact(shape, dtype, ctas, b_layout):
+    # variant 3: Combine A inside the GEMM producer path (the one or two
+    # nonzero A blocks of U_r are loaded by TMA and summed in shared memory
+    # before the MMAs); exact against the int64 oracle, whole and split groups
+    _exact_case(*shape, "strassen", dtype=dtype, b_layout=b_layout, variant="producer", num_ctas=ctas)
+
+
+def test_producer_fused_rejects():
+    # non-dividing M / K, or more than two A blocks per product (Laderman)
+    for args in ((1000, 512, 512, "strassen"), (512, 512, 520, "strassen"), (768, 768, 768, "laderman")):
+        with pytest.raises(L.LcmaError):
+            L.Plan(args[0], args[1], args[2], algo=args[3], variant="producer")
