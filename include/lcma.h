@@ -75,12 +75,14 @@ typedef enum {
                                   combines, GEMM + Combine H fused       */
     LCMA_VARIANT_PRODUCER = 3, /* Combine A in the GEMM producer path (TMA loads of
                                   the nonzero A blocks of U_r, summed in shared
-                                  memory before the MMAs), Combine B materialised
-                                  (or B~ offline), Combine H fused.  Needs <= 2 A
-                                  blocks per product (Strassen), 16-bit data and
-                                  M, K tiled exactly by the m x k block grid, else
-                                  LCMA_ERR_NOT_SUPPORTED.  Measured 3x slower than
-                                  FUSED_H on B200 (DESIGN.md s.7); never AUTO.    */
+                                  memory before the MMAs); Combine B too when B is
+                                  passed per call, stored N x K and N, K are tiled
+                                  exactly (else B~ materialised / offline);
+                                  Combine H fused.  Needs <= 2 blocks per product
+                                  (Strassen), 16-bit data and M, K tiled exactly
+                                  by the block grid, else LCMA_ERR_NOT_SUPPORTED.
+                                  Measured 3-4.6x slower than FUSED_H on B200
+                                  (DESIGN.md s.7); never chosen by AUTO.          */
     LCMA_VARIANT_TWO_LEVEL = 4 /* two-level scheme (Strassen^2 = Strassen o Strassen,
                                   P:663): combines of the composed scheme, then one
                                   fused-Combine-H GEMM per outer product writing the

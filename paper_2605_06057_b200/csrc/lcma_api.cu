@@ -622,7 +622,7 @@ lcma_status check_launch(const char* what) {
     return LCMA_OK;
 }
 
-template <int CG, int BN, int QF = 0, bool REGH = false, bool PF = false>
+template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0>
 lcma_status ensure_smem_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
@@ -737,7 +737,7 @@ lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cuda
 // tcgen05 GEMM: classical (R == 1 over A, B) or the LCMA GEMM stage over the
 // materialised At / Bt with the fused Combine H (or H store) epilogue.
 lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, void* C, float* P,
-                        int* flags, float* H, cudaStream_t st, bool pf = false) {
+                        int* flags, float* H, cudaStream_t st, int pf = 0) {
     const Scheme& S = p->sch;
     const bool classical = p->scheme_id == SCHEME_CLASSICAL;
     // QF: the shared-memory partial home covers both column halves (3 operand
@@ -751,7 +751,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     // the one without (no 128 live registers reserved in the epilogue)
     const bool regh = !classical && !H && p->cg == 2 && p->bn == 256;
     if (pf) qf = 0;
-    lcma_status rs = pf ? ensure_smem_attr<2, 256, 0, true, true>()
+    lcma_status rs = pf == 2 ? ensure_smem_attr<2, 256, 0, true, 2>()
+                   : pf == 1 ? ensure_smem_attr<2, 256, 0, true, 1>()
                    : p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
                                                 : (qf ? ensure_smem_attr<2, 256, 1, true>()
                                                       : regh ? ensure_smem_attr<2, 256, 0, true>()
@@ -768,9 +769,9 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     if (rs != LCMA_OK) return rs;
     const bool b_mn = p->d.b_layout == 0;
     bool b3d = false;
-    if (!b_mn) {   // N x K (K-major)
-        const uint64_t cols = classical ? p->d.K : p->Kb;
-        const uint64_t rows = classical ? p->d.N : (uint64_t)S.R * p->Nb;
+    if (!b_mn) {   // N x K (K-major); PF 2: the raw B, its blocks are combined in the kernel
+        const uint64_t cols = (classical || pf == 2) ? p->d.K : p->Kb;
+        const uint64_t rows = (classical || pf == 2) ? p->d.N : (uint64_t)S.R * p->Nb;
         rs = make_map(&tb, Bop, dt, cols, rows, epr, p->bn / p->cg);
     } else {       // K x N (MN-major): boxes of 128 bytes of N x BK rows
         const uint64_t cols = classical ? p->d.N : p->Nb;
@@ -925,9 +926,27 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
                     else { g.pf_blk1[r] = (int8_t)(a * S.k + b); g.pf_s1[r] = (int8_t)v; }
                 }
         }
+        g.ngrid = S.n;
+        g.pf_Nb = (int)p->Nb;
+        for (int r = 0; r < S.R; ++r) {
+            g.pfb_blk0[r] = g.pfb_blk1[r] = -1;
+            g.pfb_s0[r] = g.pfb_s1[r] = 0;
+            for (int a = 0; a < S.k; ++a)
+                for (int b = 0; b < S.n; ++b) {
+                    const int v = S.v(r, a, b);
+                    if (!v || pf != 2) continue;
+                    if (g.pfb_blk0[r] < 0) { g.pfb_blk0[r] = (int8_t)(a * S.n + b); g.pfb_s0[r] = (int8_t)v; }
+                    else { g.pfb_blk1[r] = (int8_t)(a * S.n + b); g.pfb_s1[r] = (int8_t)v; }
+                }
+        }
         g.debug &= ~(16 | 32 | 64);   // stale-operand / extra-load diagnostics do not apply
-        cfg.dynamicSmemBytes = Cfg<2, 256, 0, false, true>::kSmemBytes;
-        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, true>, ta, tb, g);
+        if (pf == 2) {
+            cfg.dynamicSmemBytes = Cfg<2, 256, 0, false, 2>::kSmemBytes;
+            e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 2>, ta, tb, g);
+        } else {
+            cfg.dynamicSmemBytes = Cfg<2, 256, 0, false, 1>::kSmemBytes;
+            e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 1>, ta, tb, g);
+        }
     } else if (p->cg == 2 && p->bn == 256 && qf) {
         cfg.dynamicSmemBytes = Cfg<2, 256, 1>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 1, true>, ta, tb, g);
@@ -1013,7 +1032,23 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
         rs = launch_combine(p, A, At, false, st);                  // Combine A (Eq. 3)
         if (rs != LCMA_OK) return rs;
     }
-    if (!Bt) {
+    // variant 3: Combine B joins Combine A in the producer path when B is
+    // given per call, stored N x K, tiled exactly and <= 2 B blocks per product
+    int pf = 0;
+    if (p->variant == LCMA_VARIANT_PRODUCER) {
+        pf = 1;
+        const Scheme& S = p->sch;
+        bool two = p->d.b_layout == 1 && !Bt_user && p->d.N == (int64_t)S.n * p->Nb &&
+                   p->d.K == (int64_t)S.k * p->Kb && !std::getenv("LCMA_PF_A_ONLY");
+        for (int r = 0; r < S.R && two; ++r) {
+            int nz = 0;
+            for (int a = 0; a < S.k; ++a)
+                for (int b = 0; b < S.n; ++b) nz += S.v(r, a, b) != 0;
+            two = nz >= 1 && nz <= 2;
+        }
+        if (two) pf = 2;
+    }
+    if (!Bt && pf != 2) {
         rs = launch_combine(p, B, w + p->off_Bt, true, st);        // Combine B (Eq. 4)
         if (rs != LCMA_OK) return rs;
         Bt = w + p->off_Bt;
@@ -1055,9 +1090,9 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
         if (rs != LCMA_OK) return rs;
         return launch_combine_h(p, H, C, st);
     }
-    if (p->variant == LCMA_VARIANT_PRODUCER)   // Combine A (Eq. 3) inside the GEMM's producer path
-        return launch_umma(p, A, Bt, C, reinterpret_cast<float*>(w + p->off_P),
-                           reinterpret_cast<int*>(w + p->off_flags), nullptr, st, true);
+    if (p->variant == LCMA_VARIANT_PRODUCER)   // Combine A (and B) inside the GEMM's producer path
+        return launch_umma(p, A, pf == 2 ? B : Bt, C, reinterpret_cast<float*>(w + p->off_P),
+                           reinterpret_cast<int*>(w + p->off_flags), nullptr, st, pf);
     return launch_umma(p, At, Bt, C, reinterpret_cast<float*>(w + p->off_P),
                        reinterpret_cast<int*>(w + p->off_flags), nullptr, st);
 }

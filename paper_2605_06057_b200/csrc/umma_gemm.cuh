@@ -60,15 +60,17 @@ constexpr int kMaxMN = 32;
 #endif
 // NP: no shared-memory partial area (the classical / unfused instantiation of
 // the 256-column pair kernel), so the ring may use that space.
-// PF: producer-fused Combine A (variant 3): a staging slot per stage for the
+// PF: producer-fused combines (variant 3): 1 = Combine A, 2 = Combine A and B;
+// a staging slot per stage for the second source block of each, and
 // second A source block, no shared-memory partial area.
-template <int CG, int BN = kBN, int QF = 0, bool NP = false, bool PF = false>
+template <int CG, int BN = kBN, int QF = 0, bool NP = false, int PF = 0>
 struct Cfg {
     static constexpr int kTileM = kBM * CG;                  // rows per group tile
     static constexpr int kBNc = BN / CG;                     // B columns staged per CTA
     static constexpr int kABytes = kBM * 128;                // 128 rows x 128 bytes
     static constexpr int kBBytes = kBNc * 128;               // kBNc x 128 B (K-major) or chunks (MN-major)
-    static constexpr int kStageBytes = kABytes + kBBytes + (PF ? kABytes : 0);   // PF: + A staging
+    static constexpr int kStageBytes =
+        kABytes + kBBytes + (PF ? kABytes : 0) + (PF == 2 ? kBBytes : 0);   // PF: + staging
     // one C_ij partial kept in shared memory (fused Combine H, whole groups):
     // 128 rows x BN (QF) or BN/2 (column half 0) fp32
     static constexpr int kPartialSmem = (NP || PF) ? 0 : kBM * (QF ? BN : BN / 2) * 4;
@@ -140,6 +142,10 @@ struct GemmParams {
     int kgrid;             // scheme k
     int pf_Kb;             // block extent along K (columns of a source block)
     int8_t pf_blk0[kMaxR], pf_blk1[kMaxR], pf_s0[kMaxR], pf_s1[kMaxR];
+    // PF = 2: Bt_r = s0 * B_blk0 + s1 * B_blk1, blocks l*n + j of the raw B
+    // (stored N x K: block (l, j) at rows j*Nb, columns l*Kb)
+    int ngrid, pf_Nb;
+    int8_t pfb_blk0[kMaxR], pfb_blk1[kMaxR], pfb_s0[kMaxR], pfb_s1[kMaxR];
     int qslot;             // QF = 0: L2 slot of the column half 1 of the HOME_SMEM partial
     int8_t home[kMaxMN];   // whole groups: C_ij partial home (HOME_REG, HOME_SMEM, or L2 slot >= 0)
     int8_t rperm[kMaxR];   // product processing order inside a group (t -> r)
@@ -374,7 +380,7 @@ __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, unsig
 }
 
 // ------------------------------------------------------------ the kernel
-template <int CG, int BN, int QF = 0, bool REGH = false, bool PF = false>
+template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
@@ -497,7 +503,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // i.e. the L2 operand traffic of an A-multicast cluster of 2 pairs
                             const bool skip_a = (p.debug & 64) && (kb & 1);
                             if (leader) {
-                                if constexpr (PF) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kBBytes * CG);
+                                if constexpr (PF == 2) ptx::mbar_arrive(&full_bar[stage]);   // all bytes on ld_bar
+                                else if constexpr (PF == 1) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kBBytes * CG);
                                 else
                                     ptx::mbar_arrive_expect_tx(&full_bar[stage],
                                                                (C_::kStageBytes - (skip_a ? C_::kABytes : 0) +
@@ -516,7 +523,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 // the local ld_bar; the combine warps sum them
                                 const int b0 = p.pf_blk0[r], b1 = p.pf_blk1[r];
                                 const int xr = x * C_::kTileM + (int)rank * kBM;
-                                ptx::mbar_arrive_expect_tx(&ld_bar[stage], (b1 >= 0 ? 2 : 1) * C_::kABytes);
+                                int ld_bytes = (b1 >= 0 ? 2 : 1) * C_::kABytes;
+                                if constexpr (PF == 2) ld_bytes += (p.pfb_blk1[r] >= 0 ? 2 : 1) * C_::kBBytes;
+                                ptx::mbar_arrive_expect_tx(&ld_bar[stage], ld_bytes);
                                 ptx::tma_load_2d(sa, &tmap_a, &ld_bar[stage], (b0 % p.kgrid) * p.pf_Kb + kcol,
                                                  (b0 / p.kgrid) * (int)p.Mb + xr);
                                 if (b1 >= 0)
@@ -525,7 +534,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                             } else if (!skip_a) {
                                 ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row, ohint, opol);
                             }
-                            if (!p.b_mn_major) {
+                            if constexpr (PF == 2) {
+                                // Combine B in the producer path: this CTA's B-half of the
+                                // one or two nonzero B blocks, on the local ld_bar
+                                const int c0 = p.pfb_blk0[r], c1 = p.pfb_blk1[r];
+                                ptx::tma_load_2d(sb, &tmap_b, &ld_bar[stage], (c0 / p.ngrid) * p.pf_Kb + kcol,
+                                                 (c0 % p.ngrid) * p.pf_Nb + b_col0);
+                                if (c1 >= 0)
+                                    ptx::tma_load_2d(sa + 2 * C_::kABytes + C_::kBBytes, &tmap_b, &ld_bar[stage],
+                                                     (c1 / p.ngrid) * p.pf_Kb + kcol, (c1 % p.ngrid) * p.pf_Nb + b_col0);
+                            } else if (!p.b_mn_major) {
                                 ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol_b);
                             } else if (p.b_3d) {
                                 ptx::tma_load_3d_cg2(sb, &tmap_b, lbar, 0, r * p.b_rows_per_r + kcol,
@@ -641,14 +659,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int r = product_at(p, u, t);
                     const float s0 = (float)p.pf_s0[r], s1 = (float)p.pf_s1[r];
                     const bool two = p.pf_blk1[r] >= 0;
+                    const float t0 = PF == 2 ? (float)p.pfb_s0[r] : 1.f, t1 = PF == 2 ? (float)p.pfb_s1[r] : 0.f;
+                    const bool twob = PF == 2 && p.pfb_blk1[r] >= 0;
                     for (int kb = 0; kb < p.nK; ++kb) {
                         ptx::mbar_wait(&ld_bar[stage], phase);
-                        if (two || s0 < 0.f) {
-                            uint8_t* sa = smem + stage * C_::kStageBytes;
-                            const uint8_t* sx = sa + C_::kABytes + C_::kBBytes;
-                            for (int q = ct; q < C_::kABytes / 16; q += 64) {
-                                uint4 a = *reinterpret_cast<const uint4*>(sa + q * 16);
-                                uint4 b = two ? *reinterpret_cast<const uint4*>(sx + q * 16) : make_uint4(0, 0, 0, 0);
+                        uint8_t* sa = smem + stage * C_::kStageBytes;
+                        bool wrote = false;
+                        // A: slot = s0 * slot + s1 * staging; B (PF 2): the same on the B slot
+                        for (int op = 0; op < (PF == 2 ? 2 : 1); ++op) {
+                            const bool pair = op == 0 ? two : twob;
+                            const float w0 = op == 0 ? s0 : t0, w1 = op == 0 ? s1 : t1;
+                            if (!pair && w0 > 0.f) continue;
+                            uint8_t* dst = op == 0 ? sa : sa + C_::kABytes;
+                            const uint8_t* sx = op == 0 ? sa + C_::kABytes + C_::kBBytes
+                                                        : sa + 2 * C_::kABytes + C_::kBBytes;
+                            const int nq = (op == 0 ? C_::kABytes : C_::kBBytes) / 16;
+                            for (int q = ct; q < nq; q += 64) {
+                                uint4 a = *reinterpret_cast<const uint4*>(dst + q * 16);
+                                uint4 b = pair ? *reinterpret_cast<const uint4*>(sx + q * 16) : make_uint4(0, 0, 0, 0);
                                 uint32_t* pa = reinterpret_cast<uint32_t*>(&a);
                                 const uint32_t* pb = reinterpret_cast<const uint32_t*>(&b);
 #pragma unroll
@@ -657,20 +685,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     if (bf16) {
                                         fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pa[h]));
                                         fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pb[h]));
-                                        __nv_bfloat162 o = __floats2bfloat162_rn(s0 * fa.x + s1 * fb.x, s0 * fa.y + s1 * fb.y);
+                                        __nv_bfloat162 o = __floats2bfloat162_rn(w0 * fa.x + w1 * fb.x, w0 * fa.y + w1 * fb.y);
                                         pa[h] = *reinterpret_cast<uint32_t*>(&o);
                                     } else {
                                         fa = __half22float2(*reinterpret_cast<const __half2*>(&pa[h]));
                                         fb = __half22float2(*reinterpret_cast<const __half2*>(&pb[h]));
-                                        __half2 o = __floats2half2_rn(s0 * fa.x + s1 * fb.x, s0 * fa.y + s1 * fb.y);
+                                        __half2 o = __floats2half2_rn(w0 * fa.x + w1 * fb.x, w0 * fa.y + w1 * fb.y);
                                         pa[h] = *reinterpret_cast<uint32_t*>(&o);
                                     }
                                 }
-                                *reinterpret_cast<uint4*>(sa + q * 16) = a;
+                                *reinterpret_cast<uint4*>(dst + q * 16) = a;
                             }
-                            // generic-proxy writes -> visible to the tensor core (async proxy)
-                            ptx::fence_proxy_async_smem();
+                            wrote = true;
                         }
+                        // generic-proxy writes -> visible to the tensor core (async proxy)
+                        if (wrote) ptx::fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive_cluster(full_leader0 + stage * 8);
                         if (++stage == kStages) { stage = 0; phase ^= 1; }

@@ -374,11 +374,13 @@ def test_partial_homes_exact(monkeypatch, env, algo, shape, ctas):
 
 @pytest.mark.parametrize("b_layout", [0, 1])
 @pytest.mark.parametrize("shape,dtype,ctas", [((512, 512, 512), 0, 0), ((1024, 1560, 768), 0, 0),
-                                              ((1536, 2304, 512), 0, 10), ((1024, 1032, 768), 1, 0)])
+                                              ((1536, 2304, 512), 0, 10), ((1024, 1032, 768), 1, 0),
+                                              ((1024, 1024, 1024), 1, 0), ((1536, 2048, 512), 0, 10)])
 def test_producer_fused_combine_a_exact(shape, dtype, ctas, b_layout):
-    # variant 3: Combine A inside the GEMM producer path (the one or two
-    # nonzero A blocks of U_r are loaded by TMA and summed in shared memory
-    # before the MMAs); exact against the int64 oracle, whole and split groups
+    # variant 3: Combine A (and, for B stored N x K with exactly tiled N, K,
+    # Combine B) inside the GEMM producer path: the one or two nonzero blocks
+    # are loaded by TMA and summed in shared memory before the MMAs; exact
+    # against the int64 oracle, whole and split groups
     _exact_case(*shape, "strassen", dtype=dtype, b_layout=b_layout, variant="producer", num_ctas=ctas)
 
 
