@@ -223,3 +223,16 @@ def test_b200_model_two_level_and_partial_terms():
     assert L.Plan(16384, 14336, 14336, dtype=L.TF32, algo="auto").info["scheme"].startswith("strassen-2x2x2")
     # 16-bit cfg2: classical (measured best)
     assert L.Plan(M, N, K, dtype=L.BF16, algo="auto").info["scheme"] == "classical"
+
+
+def test_producer_variant_plan_rules():
+    # variant 3 (Combine A / B in the GEMM producer path, include/lcma.h):
+    # Strassen on exactly tiled M, K plans; ragged M or K, or a scheme with
+    # more than two A blocks in a product (Laderman), is rejected up front
+    p = L.Plan(512, 512, 512, algo="strassen", variant="producer")
+    assert p.info["variant"] == L.VARIANT["producer"] and p.info["cta_group"] == 2
+    assert p.info["partial_slots"] == 2
+    for M, N, K, algo in ((1000, 512, 512, "strassen"), (512, 512, 520, "strassen"), (768, 768, 768, "laderman")):
+        with pytest.raises(L.LcmaError) as e:
+            L.Plan(M, N, K, algo=algo, variant="producer")
+        assert "NOT_SUPPORTED" in str(e.value)
