@@ -1,7 +1,8 @@
 """Execution-Module ablation on B200 (the paper's step-wise
 study P:475-491): Alg. 1 -> Group-Parallel -> Split-Group -> Cache-Aware ->
-product order, plus two diagnostics (mainloop only; producer-side combine
-traffic).  Interleaved timing (median of rounds).
+product order (partials in L2) -> on-chip partial homes (registers, shared
+memory), the producer-fused combine variant, plus diagnostics (mainloop only;
+producer-side combine traffic).  Interleaved timing (median of rounds).
 
 usage: python tools/ablation.py [M N K] [--static]   -> JSON on stdout
        ABL_ONE=<name> python tools/ablation.py ...   -> one launch (for ncu)
@@ -24,7 +25,10 @@ STEPS = {
     "group_parallel": (dict(algo=ALGO, schedule=3), {"LCMA_ORDER": "0", "LCMA_DISCARD": "0"}),
     "split_group_paper": (dict(algo=ALGO, schedule=2), {"LCMA_ORDER": "0", "LCMA_DISCARD": "0"}),
     "cache_aware_lockstep": (dict(algo=ALGO, schedule=1), {"LCMA_ORDER": "0", "LCMA_DISCARD": "0"}),
-    "product_order_slots_discard": (dict(algo=ALGO, schedule=1), {}),
+    "product_order_slots_discard": (dict(algo=ALGO, schedule=1),
+                                    {"LCMA_REG_PARTIAL": "0", "LCMA_SMEM_PARTIAL": "0"}),
+    "onchip_partial_homes": (dict(algo=ALGO, schedule=1), {}),
+    "variant3_producer_combine": (dict(algo=ALGO, variant="producer"), {}),
     "diag_mainloop_only": (dict(algo=ALGO), {"LCMA_DEBUG": "1"}),
     "diag_producer_combine_traffic": (dict(algo=ALGO), {"LCMA_DEBUG": "33"}),
     "diag_classical_mainloop_only": (dict(algo="classical"), {"LCMA_DEBUG": "1"}),
