@@ -197,6 +197,11 @@ int lcma_debug_stats(unsigned long long* host, int n);
  * chip (epilogue registers; shared memory for column half 0), for a scheme
  * id; *live (if non-NULL) receives the partials live at once per CTA. */
 double lcma_debug_l2_partial_tiles(int32_t scheme_id, int32_t* live);
+/* Diagnostics (LCMA_TIMELINE=1 in the environment): copies n entries of the
+ * per-product timeline of the last tcgen05 GEMM launch ([cta][512][4]
+ * globaltimer ns: MMA slot acquired, MMA issue done, epilogue has the
+ * accumulator, epilogue released it) to host memory; returns 0 on success. */
+int lcma_debug_timeline(unsigned long long* host, long long n);
 
 /* Thread-local message for the last error on this thread ("" if none). */
 const char* lcma_last_error(void);

@@ -615,6 +615,17 @@ unsigned long long* lcma_debug_stats_buffer() {
     return g_stats;
 }
 
+// per-product timeline (LCMA_TIMELINE=1); read back with lcma_debug_timeline().
+unsigned long long* g_tl = nullptr;
+unsigned long long* lcma_debug_timeline_buffer() {
+    if (!g_tl) {
+        const size_t bytes = (size_t)1024 * kTlMax * 4 * sizeof(unsigned long long);
+        if (cudaMalloc(&g_tl, bytes) != cudaSuccess) { cudaGetLastError(); g_tl = nullptr; }
+        else cudaMemset(g_tl, 0, bytes);
+    }
+    return g_tl;
+}
+
 lcma_status check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -824,6 +835,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     if (const char* oh = std::getenv("LCMA_OPERAND_HINT")) g.operand_hint = std::atoi(oh);
     if (const char* sw = std::getenv("LCMA_SWZ")) g.swz = std::max(1, std::atoi(sw));
     if (std::getenv("LCMA_STATS")) g.stats = lcma_debug_stats_buffer();
+    if (std::getenv("LCMA_TIMELINE")) g.tl = lcma_debug_timeline_buffer();
     const int mn = S.m * S.n;
     if (S.R > kMaxR || mn > kMaxMN) return fail(LCMA_ERR_NOT_SUPPORTED, "scheme too large for the fused kernel");
     for (int r = 0; r < S.R; ++r) {
@@ -1139,6 +1151,13 @@ extern "C" void lcma_set_kernel_events(void* ev_start, void* ev_end) {
 
 // Diagnostics: co-resident clusters of `cluster_size` CTAs for the tcgen05
 // GEMM kernel configuration (cudaOccupancyMaxActiveClusters); -1 on error.
+// Diagnostics (LCMA_TIMELINE=1): copies n entries of the per-product timeline
+// ([cta][512][4] globaltimer ns) to host memory; 0 on success.
+extern "C" int lcma_debug_timeline(unsigned long long* host, long long n) {
+    if (!g_tl) return -1;
+    return cudaMemcpy(host, g_tl, (size_t)n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -1;
+}
+
 // Diagnostics: fused Combine-H partial tile transfers per group that go to L2
 // (the on-chip homes excluded) and live partials per CTA, for scheme_id.
 extern "C" double lcma_debug_l2_partial_tiles(int32_t scheme_id, int32_t* live) {

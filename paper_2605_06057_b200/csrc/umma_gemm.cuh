@@ -51,6 +51,12 @@ constexpr int kEpiWarp0 = 4;      // first epilogue warp
 constexpr int kEpiWarps = 8;
 constexpr int kMaxR = 128;
 constexpr int kMaxMN = 32;
+constexpr int kTlMax = 512;       // timeline entries per CTA
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // QF = 1: the shared-memory C_ij partial covers the whole 128 x BN slab of
 // the CTA (128 KB for BN = 256, leaving room for 3 operand stages); QF = 0:
@@ -123,6 +129,9 @@ struct GemmParams {
     int b_layout_type;     // UMMA smem layout of B (2 = SWIZZLE_128B, 1 = 128B_BASE32B)
     int b_sbo;             // B stride byte offset (8-row (or 4-row) K group stride)
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics)
+    unsigned long long* tl;      // optional per-product timeline (diagnostics): [cta][kTlMax][4] globaltimer ns:
+                                 // 0 MMA slot acquired, 1 MMA issue done, 2 epilogue (half 0) has the
+                                 // accumulator, 3 epilogue (half 1) released it
     int m, n;              // scheme grid (C blocks)
     long long M, N;        // true C extents (crop)
     long long Mb, Nb;      // block extents: C_ij origin = (i*Mb, j*Nb)
@@ -588,10 +597,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long t_start = clock64();
             UnitIter it(p, w);
             Unit u;
+            int tli = 0;
             while (it.next(u)) {
                 for (int r = u.r0; r < u.r1; ++r) {
                     timed_wait(&tempty_bar[acc], acc_phase ^ 1, (p.stats && lane == 0) ? &w_tempty : nullptr);
                     ptx::tc_fence_after();
+                    if (p.tl && lane == 0 && tli < kTlMax) p.tl[((size_t)blockIdx.x * kTlMax + tli) * 4 + 0] = gtimer();
                     const uint32_t d_tmem = tmem_base + acc * BN;
                     for (int kb = 0; kb < p.nK; ++kb) {
                         timed_wait(&full_bar[stage], phase, (p.stats && lane == 0) ? &w_full : nullptr);
@@ -631,6 +642,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else ptx::mma_commit_cg2_mc(&tfull_bar[acc], 0x3);
                     }
                     __syncwarp();
+                    if (p.tl && lane == 0 && tli < kTlMax) p.tl[((size_t)blockIdx.x * kTlMax + tli) * 4 + 1] = gtimer();
+                    ++tli;
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
             }
@@ -727,6 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // classical and unfused GEMMs keep the register budget)
         constexpr int kPregCols = REGH ? BN / 2 : 1;
         float preg[kPregCols];
+        int tl_i = 0;             // timeline product index (diagnostics)
         UnitIter it(p, w);
         Unit u;
         while (it.next(u)) {
@@ -746,6 +760,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (p.debug & 8) ptx::mbar_wait_sleep(&tfull_bar[acc], acc_phase, 256);
                 else timed_wait(&tfull_bar[acc], acc_phase, (p.stats && ew == 0 && lane == 0) ? &w_tfull : nullptr);
                 ptx::tc_fence_after();
+                if (p.tl && ew == 0 && lane == 0 && tl_i < kTlMax) p.tl[((size_t)blockIdx.x * kTlMax + tl_i) * 4 + 2] = gtimer();
                 const uint32_t t_addr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
                                         (uint32_t)(acc * BN + half * (BN / 2));
                 const uint32_t nz = p.nzmask[r];
@@ -777,6 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if constexpr (CG == 1) ptx::mbar_arrive_relaxed(&tempty_bar[acc]);
                             else ptx::mbar_arrive_cluster_relaxed(tempty_leader0 + acc * 8);
                         }
+                        if (p.tl && ew == 4 && lane == 0 && tl_i < kTlMax) p.tl[((size_t)blockIdx.x * kTlMax + tl_i) * 4 + 3] = gtimer();
                     }
                     if (p.debug & 1) return;
                     const int c4 = (col_base + ch * 32) >> 2;     // first float4 column of the chunk
@@ -916,6 +932,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     chunk(std::integral_constant<int, 3>{});
                 }
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                ++tl_i;
                 seen |= nz;
             }
             if (p.epi_mode != EPI_FUSED || u.role == ROLE_WHOLE || (p.debug & 1)) continue;
