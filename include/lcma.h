@@ -26,7 +26,12 @@
  *    the CUDA error string in lcma_last_error(); asynchronous faults surface
  *    at the caller's next synchronisation.
  *  - The workspace must be zero-filled once before its first use (the
- *    library keeps its split-group flags at zero between calls).
+ *    library keeps its schedule counter and split-group flags at zero between
+ *    calls).  A workspace may be used by ONE in-flight call at a time (two
+ *    streams need two workspaces).  If a launch fails or is aborted mid-way
+ *    (LCMA_ERR_CUDA, a device fault), zero the workspace again before reuse.
+ *  - The tcgen05 GEMM is a persistent kernel sized to the device's co-resident
+ *    CTA pairs; the plan is bound to the device current at lcma_plan* time.
  *  - Results are bitwise deterministic for a fixed plan: no floating-point
  *    atomics; split groups merge in a fixed order (reading 10).
  */
@@ -110,14 +115,24 @@ typedef struct {
     int32_t b_layout;         /* 0: B is K x N (paper), 1: B is N x K              */
     int32_t b_static;         /* 1: lcma_gemm_precombined will be used     */
     int32_t variant;          /* lcma_variant                                      */
-    int32_t schedule;         /* 0 auto, 1 lockstep rounds + split tail (cache-aware),
-                                 2 paper's contiguous split-group order,
-                                 3 whole groups only (group-parallel, no split)   */
+    int32_t schedule;         /* 0 auto = 1; 1 cache-aware: whole groups handed out
+                                 in raster order at run time (ticket counter in the
+                                 workspace, so the groups in flight stay a compact
+                                 window of the raster) + the split tail;
+                                 2 paper's contiguous split-group order;
+                                 3 whole groups only (group-parallel, no split);
+                                 4 static lockstep rounds (group w + i*W to unit w)
+                                   + split tail (round-1 schedule, ablation)       */
     int32_t num_ctas;         /* 0 = one per SM                                    */
     const lcma_hw_profile* hw;/* NULL -> built-in B200 profile                     */
     int32_t decision_model;   /* algo AUTO: 0 = this build's B200-calibrated model
                                  (reading 19), 1 = the paper's model
                                  verbatim (as lcma_decide)              */
+    /* tuning (0 = the measured default for the shape; results are identical
+       for every value, only the time changes) */
+    int32_t prefetch_kblocks; /* L2 prefetch of operand tiles this many 64-element
+                                 k-blocks ahead of their TMA load; < 0: off        */
+    int32_t raster_rows;      /* group raster: band height in tile rows            */
 } lcma_plan_desc;
 
 typedef struct {

@@ -418,6 +418,54 @@ def lcma_f64(A, B, s: Scheme, extents=None, fmt_in=None, fmt_h=None, fmt_out=Non
     return LcmaResult(C, At, Bt, H, dict(zip(_COUNTER_NAMES, (int(c) for c in cnt))))
 
 
+def lcma_rows_f64(A, B, s: Scheme, rows, extents=None, fmt_in=None, fmt_out=None) -> np.ndarray:
+    """Rows `rows` of Algorithm 1 with the dtype-faithful rounding
+    points of lcma_f64 (fmt_in after Combine A / B, fmt_out on C; H and the
+    Combine-H sums in fp64): for sampled checks at full size, where the whole
+    evaluator would take minutes.  Output row rho = i*Mb + x only needs row x
+    of every A~_r (Eq. 3) and all of B~_r (Eq. 4); H_r[x, :]
+    (Eq. 5) is a library matmul step; Combine H is Eq. 6.
+    Zero padding outside M x K / K x N."""
+    A = np.asarray(A, np.float64)
+    B = np.asarray(B, np.float64)
+    M, K = A.shape
+    N = B.shape[1]
+    Mb, Kb, Nb = extents if extents else default_extents(M, N, K, s)
+    Ap = np.zeros((s.m * Mb, s.k * Kb))
+    Ap[:M, :K] = A
+    Bp = np.zeros((s.k * Kb, s.n * Nb))
+    Bp[:K, :N] = B
+    rows = np.asarray(rows, np.int64)
+    out = np.zeros((len(rows), N))
+    Bt = []
+    for r in range(s.R):                                   # Combine B (Eq. 4)
+        acc = np.zeros((Kb, Nb))
+        for l in range(s.k):
+            for j in range(s.n):
+                if s.V[r, l, j]:
+                    acc += s.V[r, l, j] * Bp[l * Kb:(l + 1) * Kb, j * Nb:(j + 1) * Nb]
+        Bt.append(round_to(acc, fmt_in) if fmt_in else acc)
+    for q, rho in enumerate(rows):
+        i, x = divmod(int(rho), Mb)
+        crow = np.zeros(s.n * Nb)
+        for r in range(s.R):
+            if not s.W[r, i, :].any():
+                continue
+            at = np.zeros(Kb)                                # Combine A (Eq. 3), row x
+            for i2 in range(s.m):
+                for l in range(s.k):
+                    if s.U[r, i2, l]:
+                        at += s.U[r, i2, l] * Ap[i2 * Mb + x, l * Kb:(l + 1) * Kb]
+            if fmt_in:
+                at = round_to(at, fmt_in)
+            h = at @ Bt[r]                                   # Eq. 5, row x of H_r
+            for j in range(s.n):                             # Eq. 6
+                if s.W[r, i, j]:
+                    crow[j * Nb:(j + 1) * Nb] += s.W[r, i, j] * h
+        out[q] = crow[:N]          # C_ij holds columns j*Nb .. j*Nb+Nb-1: crop to N
+    return round_to(out, fmt_out) if fmt_out else out
+
+
 def lcma_i64(A, B, s: Scheme, extents=None, intermediates=False) -> LcmaResult:
     """Algorithm 1 in exact int64 (exact mode)."""
     A = np.ascontiguousarray(A, np.int64)

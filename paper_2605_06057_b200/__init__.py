@@ -42,7 +42,8 @@ class PlanDesc(ctypes.Structure):
                 ("scheme_id", ctypes.c_int32), ("b_layout", ctypes.c_int32),
                 ("b_static", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("schedule", ctypes.c_int32), ("num_ctas", ctypes.c_int32),
-                ("hw", ctypes.POINTER(HwProfile)), ("decision_model", ctypes.c_int32)]
+                ("hw", ctypes.POINTER(HwProfile)), ("decision_model", ctypes.c_int32),
+                ("prefetch_kblocks", ctypes.c_int32), ("raster_rows", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -136,11 +137,13 @@ def _torch_dtype(code):
 
 
 class Plan:
-    """lcma_plan_ex wrapper.  gemm() takes CUDA torch tensors (row-major)."""
+    """lcma_plan_ex wrapper.  gemm() takes CUDA torch tensors (row-major,
+    contiguous, on one device, of the plan's dtype and shape); the call is
+    enqueued on that device's current stream (or `stream`)."""
 
     def __init__(self, M, N, K, dtype=BF16, algo="auto", out_dtype=None, b_layout=0,
                  variant="auto", b_static=False, schedule=0, num_ctas=0, scheme_id=0, hw=None,
-                 decision_model=0):
+                 decision_model=0, prefetch_kblocks=0, raster_rows=0):
         L = lib()
         if out_dtype is None:
             out_dtype = FP32 if dtype == TF32 else dtype
@@ -148,7 +151,7 @@ class Plan:
         d = PlanDesc(M, N, K, dtype, out_dtype, ALGO[algo] if isinstance(algo, str) else algo,
                      scheme_id, b_layout, int(b_static),
                      VARIANT[variant] if isinstance(variant, str) else variant,
-                     schedule, num_ctas, self._hw, decision_model)
+                     schedule, num_ctas, self._hw, decision_model, prefetch_kblocks, raster_rows)
         h = ctypes.c_void_p()
         _check(L.lcma_plan_ex(ctypes.byref(d), ctypes.byref(h)))
         self._h = h
@@ -159,7 +162,7 @@ class Plan:
         self.info = info.as_dict()
         self.workspace_bytes = self.info["workspace_bytes"]
         self.btilde_bytes = self.info["btilde_bytes"]
-        self._ws = None
+        self._ws = {}
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -167,46 +170,101 @@ class Plan:
             _lib.lcma_free(h)
             self._h = None
 
-    def workspace(self, device=None):
-        """Zero-initialised workspace (the library keeps its flags zero afterwards)."""
+    def workspace(self, device=None, stream=None):
+        """Zero-initialised workspace (the library keeps its counters and flags
+        zero afterwards).  Cached per (device, stream): a workspace must not be
+        used by two in-flight calls at once (include/lcma.h)."""
         import torch
-        if self._ws is None or (device is not None and self._ws.device != torch.device(device)):
-            self._ws = torch.zeros(max(self.workspace_bytes, 16), dtype=torch.uint8,
-                                   device=device or "cuda")
-        return self._ws
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        key = (dev.index, self._stream(stream, dev).value or 0)
+        ws = self._ws.get(key)
+        if ws is None:
+            ws = torch.zeros(max(self.workspace_bytes, 16), dtype=torch.uint8, device=dev)
+            self._ws[key] = ws
+        return ws
 
-    def _stream(self, stream):
+    @staticmethod
+    def _stream(stream, device=None):
         import torch
         if stream is None:
-            stream = torch.cuda.current_stream()
+            stream = torch.cuda.current_stream(device)
         return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
 
     def empty_c(self, device="cuda"):
         import torch
         return torch.empty((self.M, self.N), dtype=_torch_dtype(self.out_dtype), device=device)
 
+    # -- argument checks (the C ABI sees raw pointers and cannot check sizes)
+    def _check_t(self, t, name, dtype, numel, dev):
+        import torch
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise LcmaError(1, f"{name} must be a CUDA tensor")
+        if t.device != dev:
+            raise LcmaError(1, f"{name} is on {t.device}, A on {dev}")
+        if not t.is_contiguous():
+            raise LcmaError(1, f"{name} must be contiguous (row-major)")
+        if dtype is not None and t.dtype != dtype:
+            raise LcmaError(1, f"{name} has dtype {t.dtype}, the plan needs {dtype}")
+        if t.numel() * t.element_size() < numel:
+            raise LcmaError(1, f"{name} holds {t.numel() * t.element_size()} bytes, needs {numel}")
+
+    def _check_args(self, A, B, Bt, C, ws):
+        import torch
+        dt = _torch_dtype(self.dtype)
+        e = torch.empty((), dtype=dt).element_size()
+        self._check_t(A, "A", dt, 0, A.device if isinstance(A, torch.Tensor) else None)
+        dev = A.device
+        if tuple(A.shape) != (self.M, self.K):
+            raise LcmaError(1, f"A is {tuple(A.shape)}, the plan needs {(self.M, self.K)}")
+        if B is not None:
+            self._check_t(B, "B", dt, 0, dev)
+            want = (self.K, self.N) if self.b_layout == 0 else (self.N, self.K)
+            if tuple(B.shape) != want:
+                raise LcmaError(1, f"B is {tuple(B.shape)}, the plan needs {want}")
+        if Bt is not None:
+            self._check_t(Bt, "Bt", None, self.btilde_bytes, dev)
+        self._check_t(C, "C", _torch_dtype(self.out_dtype), 0, dev)
+        if tuple(C.shape) != (self.M, self.N):
+            raise LcmaError(1, f"C is {tuple(C.shape)}, the plan needs {(self.M, self.N)}")
+        self._check_t(ws, "workspace", None, self.workspace_bytes, dev)
+        return dev
+
     def gemm(self, A, B, C=None, workspace=None, stream=None):
+        import torch
         if C is None:
             C = self.empty_c(A.device)
-        ws = workspace if workspace is not None else self.workspace(A.device)
-        _check(lib().lcma_gemm(self._h, A.data_ptr(), B.data_ptr(), C.data_ptr(),
-                               ws.data_ptr(), ws.numel() * ws.element_size(), self._stream(stream)))
+        ws = workspace if workspace is not None else self.workspace(A.device, stream)
+        dev = self._check_args(A, B, None, C, ws)
+        with torch.cuda.device(dev):
+            _check(lib().lcma_gemm(self._h, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+                                   ws.data_ptr(), ws.numel() * ws.element_size(), self._stream(stream, dev)))
         return C
 
     def precombine_b(self, B, Bt=None, stream=None):
         import torch
+        self._check_t(B, "B", _torch_dtype(self.dtype), 0, B.device if isinstance(B, torch.Tensor) else None)
         if Bt is None:
             Bt = torch.empty(max(self.btilde_bytes, 16), dtype=torch.uint8, device=B.device)
-        _check(lib().lcma_precombine_b(self._h, B.data_ptr(), Bt.data_ptr(), self._stream(stream)))
+        self._check_t(Bt, "Bt", None, self.btilde_bytes, B.device)
+        with torch.cuda.device(B.device):
+            _check(lib().lcma_precombine_b(self._h, B.data_ptr(), Bt.data_ptr(), self._stream(stream, B.device)))
         return Bt
 
     def gemm_precombined(self, A, Bt, C=None, workspace=None, stream=None):
+        import torch
         if C is None:
             C = self.empty_c(A.device)
-        ws = workspace if workspace is not None else self.workspace(A.device)
-        _check(lib().lcma_gemm_precombined(self._h, A.data_ptr(), Bt.data_ptr(), C.data_ptr(),
-                                           ws.data_ptr(), ws.numel() * ws.element_size(),
-                                           self._stream(stream)))
+        ws = workspace if workspace is not None else self.workspace(A.device, stream)
+        if self.info["algo"] == ALGO["classical"]:
+            dev = self._check_args(A, Bt, None, C, ws)     # classical: Bt is B itself
+        else:
+            dev = self._check_args(A, None, Bt, C, ws)
+        with torch.cuda.device(dev):
+            _check(lib().lcma_gemm_precombined(self._h, A.data_ptr(), Bt.data_ptr(), C.data_ptr(),
+                                               ws.data_ptr(), ws.numel() * ws.element_size(),
+                                               self._stream(stream, dev)))
         return C
 
     def schedule(self, cta):

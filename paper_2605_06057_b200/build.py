@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblcma.so")
 SOURCES = ["lcma_api.cu", "schemes.cpp", "decision.cpp"]
-HEADERS = ["ptx.cuh", "umma_gemm.cuh", "combine.cuh", "schemes.h", "decision.h"]
+HEADERS = ["ptx.cuh", "umma_gemm.cuh", "combine.cuh", "schemes.h", "decision.h", "diag.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -37,6 +37,24 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB) -> str:
     subprocess.check_call(cmd)
     os.replace(tmp, out)
     return out
+
+
+DIAG_LIB = os.path.join(HERE, "liblcma_diag.so")
+
+
+def build_diag(force: bool = False) -> str:
+    """The -DLCMA_DIAG build (tuning / diagnostic environment knobs, see
+    csrc/diag.h): used by tests/_diag_homes.py and tools/, never by the
+    product path."""
+    if not force and os.path.exists(DIAG_LIB) and os.path.exists(LIB) and \
+            os.path.getmtime(DIAG_LIB) >= os.path.getmtime(LIB) and not _stale():
+        return DIAG_LIB
+    old = os.environ.get("LCMA_NVCC_FLAGS", "")
+    os.environ["LCMA_NVCC_FLAGS"] = (old + " -DLCMA_DIAG").strip()
+    try:
+        return build(force=True, out=DIAG_LIB)
+    finally:
+        os.environ["LCMA_NVCC_FLAGS"] = old
 
 
 if __name__ == "__main__":

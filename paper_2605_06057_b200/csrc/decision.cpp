@@ -4,6 +4,7 @@
 // stage's arithmetic intensity exceeds the device ratio, else memory time
 // (P:236-237), stages summed without overlap, argmin with classical fallback.
 #include "decision.h"
+#include "diag.h"
 
 #include <cmath>
 #include <cstdlib>
@@ -176,7 +177,7 @@ Profile default_profile(int dtype) {
     // 16-bit data and -4 % for tf32, Laderman / Strassen^2 through alpha)
     p.alpha_partial = 8.0;
     p.epi_overhead = bytes == 2.0 ? 0.08 : -0.04;
-    if (const char* env = std::getenv("LCMA_PROFILE")) {
+    if (const char* env = diag_env("LCMA_PROFILE")) {
         const char* keys[5] = {"flops_mul=", "flops_add=", "beta_elems=", "beta_combine=", "alpha_partial="};
         double* dst[5] = {&p.flops_mul, &p.flops_add, &p.beta, &p.beta_combine, &p.alpha_partial};
         for (int i = 0; i < 5; ++i) {

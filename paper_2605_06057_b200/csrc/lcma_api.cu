@@ -16,6 +16,7 @@
 #include "../../include/lcma.h"
 #include "combine.cuh"
 #include "decision.h"
+#include "diag.h"
 #include "schemes.h"
 #include "umma_gemm.cuh"
 
@@ -34,6 +35,7 @@ lcma_status fail(lcma_status st, const std::string& msg) {
 }
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+constexpr int kDefaultPrefetch = 0;    // L2 prefetch distance when the desc says 0 (auto)
 int64_t roundup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -49,14 +51,23 @@ int device_sm_count() {
     return sms;
 }
 
-// Co-resident clusters of 2 for umma_gemm_kernel<2> (0 if unknown / no GPU).
+constexpr int kMaxDev = 64;
+int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return -1; }
+    return (dev >= 0 && dev < kMaxDev) ? dev : -1;
+}
+
+// Co-resident clusters of 2 for umma_gemm_kernel<2> on the current device
+// (0 if unknown / no GPU).
 int max_active_pairs() {
-    static int cached = -1;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cached = 0;
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
+    static int cached[kMaxDev];
+    static std::once_flag once[kMaxDev];
+    const int dv = current_device();
+    if (dv < 0) return 0;
+    std::call_once(once[dv], [dv] {
+        int& c = cached[dv];
+        c = 0;
         if (cudaFuncSetAttribute(umma_gemm_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg<2, 256, 0, true>::kSmemBytes) != cudaSuccess) { cudaGetLastError(); return; }
         cudaLaunchConfig_t cfg;
@@ -72,10 +83,10 @@ int max_active_pairs() {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, umma_gemm_kernel<2, 256>, &cfg) == cudaSuccess) cached = n;
+        if (cudaOccupancyMaxActiveClusters(&n, umma_gemm_kernel<2, 256>, &cfg) == cudaSuccess) c = n;
         else cudaGetLastError();
     });
-    return cached;
+    return cached[dv];
 }
 
 }  // namespace
@@ -91,7 +102,8 @@ struct lcma_plan_s {
     int BK, e;
     int nX, nZ, G, nK;
     int ctas, cg, bn, q, tail_c, swz;
-    size_t off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
+    int n_whole, dyn, pf_dist;
+    size_t off_sched, off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
     size_t off_inner = 0;          // two-level: the inner plan's partial slots + flags
     lcma_plan_s* inner = nullptr;  // two-level: fused GEMM plan of the base scheme
     lcma_plan_info info;
@@ -108,8 +120,10 @@ std::vector<HostUnit> host_units(const lcma_plan_s* p, int w) {
     std::vector<HostUnit> out;
     const int R = p->sch.R;
     const int W = p->ctas / p->cg;
-    for (int i = 0; i < p->q && i * W + w < p->G; ++i) out.push_back({i * W + w, 0, R, ROLE_WHOLE});
-    const long long Tt = std::max<long long>(0, (long long)(p->G - (long long)p->q * W) * R);
+    // (dynamic schedules hand the n_whole whole groups out at run time; the
+    // static view below assigns them round by round)
+    for (int i = 0; i * W + w < p->n_whole; ++i) out.push_back({i * W + w, 0, R, ROLE_WHOLE});
+    const long long Tt = std::max<long long>(0, (long long)(p->G - (long long)p->n_whole) * R);
     long long t = std::min<long long>((long long)w * p->tail_c, Tt);
     long long t_end = std::min<long long>(t + p->tail_c, Tt);
     while (t < t_end) {
@@ -118,7 +132,7 @@ std::vector<HostUnit> host_units(const lcma_plan_s* p, int w) {
         long long stop = std::min<long long>((gl + 1) * R, t_end);
         int r1 = (int)(stop - gl * R);
         int role = (r0 == 0 && r1 == R) ? ROLE_WHOLE : (r0 == 0 ? ROLE_OWNER : ROLE_CONTRIB);
-        out.push_back({p->q * W + (int)gl, r0, r1, role});
+        out.push_back({p->n_whole + (int)gl, r0, r1, role});
         t = stop;
     }
     return out;
@@ -127,26 +141,35 @@ std::vector<HostUnit> host_units(const lcma_plan_s* p, int w) {
 void make_schedule(lcma_plan_s* p, int mode) {
     const int R = p->sch.R;
     const int W = p->ctas / p->cg;
+    p->dyn = 0;
     if (mode == 2) {
         p->q = 0;                              // paper: contiguous split-group chunks
     } else if (mode == 3) {
         p->q = (int)cdiv(p->G, W);             // group-parallel only: whole groups, no split
     } else {
         p->q = p->G / W;                       // lockstep rounds (cache-aware)
+        // mode 1 (default): the whole groups are handed out at run time in
+        // raster order (the pairs drift apart by a round every ~50 rounds
+        // under a static assignment, which scatters the groups in flight over
+        // the raster: tools/r02/drift.py); mode 4: static rounds
+        p->dyn = mode == 4 ? 0 : 1;
     }
-    const long long Tt = std::max<long long>(0, (long long)(p->G - (long long)p->q * W) * R);
+    p->n_whole = (int)std::min<long long>((long long)p->q * W, p->G);
+    // R == 1 (classical): nothing to split, every group is handed out whole
+    if (p->dyn && R == 1) p->n_whole = p->G;
+    const long long Tt = std::max<long long>(0, (long long)(p->G - (long long)p->n_whole) * R);
     p->tail_c = Tt > 0 ? (int)cdiv(Tt, W) : 1;
     // raster band height (tile rows): LCMA rounds touch R operand panels per
     // tile, so a lower band keeps the round's A panels L2-resident (measured
     // cfg2 Strassen -1..2 %, classical best at 16; tools/swz_exp*.sh)
-    p->swz = R > 1 ? 8 : 16;
+    p->swz = p->d.raster_rows > 0 ? p->d.raster_rows : (R > 1 ? 8 : 16);
     p->info.groups = p->G;
     p->info.tiles = (int)std::min<long long>((long long)p->G * R, INT32_MAX);
     p->info.ctas = p->ctas;
-    p->info.waves = p->q * R + (Tt > 0 ? p->tail_c : 0);
+    p->info.waves = (int)(p->dyn ? cdiv(p->n_whole, W) : p->q) * R + (Tt > 0 ? p->tail_c : 0);
     p->info.group_waves = (int)cdiv(p->G, W) * R;
     int splits = 0;
-    for (long long gl = 0; gl < p->G - p->q * W; ++gl) {
+    for (long long gl = 0; gl < p->G - p->n_whole; ++gl) {
         long long a = gl * R, b = gl * R + R - 1;
         if (a / p->tail_c != b / p->tail_c) ++splits;
     }
@@ -275,7 +298,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         const int sms = device_sm_count();
         p->ctas = d.num_ctas > 0 ? std::min(d.num_ctas, sms) : sms;
         p->cg = 2;
-        if (const char* e_cg = std::getenv("LCMA_CG")) p->cg = std::atoi(e_cg) == 1 ? 1 : 2;
+        if (const char* e_cg = diag_env("LCMA_CG")) p->cg = std::atoi(e_cg) == 1 ? 1 : 2;
         if (p->ctas < 2) p->cg = 1;
         p->ctas -= p->ctas % p->cg;
         if (p->cg == 2) {
@@ -286,7 +309,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         }
         const int tileM = kBM * p->cg;
         p->bn = kBN;
-        if (const char* e_bn = std::getenv("LCMA_BN")) p->bn = std::atoi(e_bn) == 128 ? 128 : 256;
+        if (const char* e_bn = diag_env("LCMA_BN")) p->bn = std::atoi(e_bn) == 128 ? 128 : 256;
         const int BNp = p->bn;
         if (classical) {
             p->nX = (int)cdiv(d.M, tileM);
@@ -309,7 +332,10 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             return fail(LCMA_ERR_NOT_SUPPORTED, "problem too large for 32-bit tile coordinates");
         }
         p->G = p->nX * p->nZ;
-        make_schedule(p, (d.schedule == 2 || d.schedule == 3) ? d.schedule : 1);
+        make_schedule(p, (d.schedule >= 2 && d.schedule <= 4) ? d.schedule : 1);
+        if (variant == LCMA_VARIANT_PRODUCER) p->dyn = 0;   // its combine warps walk the static schedule
+        // L2 prefetch distance (k-blocks): measured default
+        p->pf_dist = d.prefetch_kblocks < 0 ? 0 : d.prefetch_kblocks > 0 ? d.prefetch_kblocks : kDefaultPrefetch;
         if (variant == LCMA_VARIANT_PRODUCER &&
             (p->cg != 2 || p->bn != 256 || d.M != (int64_t)S.m * p->Mb || d.K != (int64_t)S.k * p->Kb)) {
             delete p;
@@ -348,8 +374,12 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
 
     // ---- workspace layout
     size_t off = 0;
-    p->off_P = p->off_flags = p->off_At = p->off_Bt = p->off_H = 0;
+    p->off_sched = p->off_P = p->off_flags = p->off_At = p->off_Bt = p->off_H = 0;
     const int mn = S.m * S.n;
+    if (d.dtype != LCMA_FP32 && variant != LCMA_VARIANT_TWO_LEVEL) {
+        p->off_sched = off;                    // dynamic-schedule ticket counter
+        off = align256(off + 256);
+    }
     if (!classical) {
         if (d.dtype != LCMA_FP32 && (variant == LCMA_VARIANT_FUSED_H || variant == LCMA_VARIANT_PRODUCER)) {
             p->off_P = off;
@@ -407,7 +437,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     I.btilde_bytes = p->bt_bytes;
     I.partial_slots = 0;
     if (!classical && d.dtype != LCMA_FP32 && (variant == LCMA_VARIANT_FUSED_H || variant == LCMA_VARIANT_PRODUCER)) {
-        const bool use_order = !std::getenv("LCMA_ORDER") || std::atoi(std::getenv("LCMA_ORDER")) != 0;
+        const bool use_order = !diag_env("LCMA_ORDER") || std::atoi(diag_env("LCMA_ORDER")) != 0;
         I.partial_slots = use_order ? scheme_product_order(p->scheme_id).nslot : S.m * S.n;
     }
     if (variant == LCMA_VARIANT_TWO_LEVEL) I.partial_slots = p->inner->info.partial_slots;
@@ -633,22 +663,28 @@ lcma_status check_launch(const char* what) {
     return LCMA_OK;
 }
 
+// The dynamic shared-memory limit is a per-device function attribute: set it
+// once per (instantiation, device).
 template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0>
 lcma_status ensure_smem_attr() {
-    static std::once_flag once;
-    static cudaError_t err = cudaSuccess;
-    std::call_once(once, [] {
-        err = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF>::kSmemBytes);
+    static std::once_flag once[kMaxDev];
+    static cudaError_t err[kMaxDev];
+    const int dv = current_device();
+    if (dv < 0) return fail(LCMA_ERR_CUDA, "no current CUDA device (or ordinal >= 64)");
+    std::call_once(once[dv], [dv] {
+        err[dv] = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF>::kSmemBytes);
     });
-    if (err != cudaSuccess) return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
+    if (err[dv] != cudaSuccess)
+        return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err[dv]));
     return LCMA_OK;
 }
 
 int grid_for(long long work, int per_block) {
     long long b = (work + per_block - 1) / per_block;
     if (b < 1) b = 1;
-    static const long long cap = std::getenv("LCMA_COMB_BLOCKS") ? std::atoll(std::getenv("LCMA_COMB_BLOCKS"))
+    static const long long cap = diag_env("LCMA_COMB_BLOCKS") ? std::atoll(diag_env("LCMA_COMB_BLOCKS"))
                                                                  : 148 * 16;
     if (b > cap) b = cap;
     return (int)b;
@@ -688,7 +724,7 @@ lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, boo
                 c.coef[r * inst + a * Q + b] = v;
             }
     const bool fp32 = c.elem == ELEM_FP32;
-    if (!fp32 && (inst == 4 || inst == 9 || inst == 16) && !std::getenv("LCMA_OLD_COMBINE")) {
+    if (!fp32 && (inst == 4 || inst == 9 || inst == 16) && !diag_env("LCMA_OLD_COMBINE")) {
         // 16-bit sources with 9 or 16 blocks: packed sources keep more loads in
         // flight (measured 1.4x / 2.3x faster than the unpacked kernel below)
         const long long nv = c.E0 * (c.E1 / 8);
@@ -748,14 +784,14 @@ lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cuda
 // tcgen05 GEMM: classical (R == 1 over A, B) or the LCMA GEMM stage over the
 // materialised At / Bt with the fused Combine H (or H store) epilogue.
 lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, void* C, float* P,
-                        int* flags, float* H, cudaStream_t st, int pf = 0) {
+                        int* flags, int* sched, float* H, cudaStream_t st, int pf = 0) {
     const Scheme& S = p->sch;
     const bool classical = p->scheme_id == SCHEME_CLASSICAL;
     // QF: the shared-memory partial home covers both column halves (3 operand
     // stages; measured slower than 4 stages with column half 1 in L2: cfg2
     // 910 vs 824 us, so opt-in only)
     int qf = 0;
-    if (const char* v = std::getenv("LCMA_QFULL"))
+    if (const char* v = diag_env("LCMA_QFULL"))
         qf = (!classical && !H && p->cg == 2 && p->bn == 256 && S.m * S.n > 1 && std::atoi(v) != 0) ? 1 : 0;
     // REGH: the instantiation with a register partial home (fused Combine H of
     // an LCMA scheme on 256-column pair tiles); classical / unfused GEMMs use
@@ -789,10 +825,10 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         const uint64_t rows = classical ? p->d.K : (uint64_t)S.R * p->Kb;
         CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
         if (dt == LCMA_TF32 || dt == LCMA_FP32) {
-            if (const char* v = std::getenv("LCMA_TF32_MN_SWZ")) swz = (CUtensorMapSwizzle)std::atoi(v);
+            if (const char* v = diag_env("LCMA_TF32_MN_SWZ")) swz = (CUtensorMapSwizzle)std::atoi(v);
             else swz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
         }
-        b3d = cols % (uint64_t)epr == 0 && !std::getenv("LCMA_B2D") &&
+        b3d = cols % (uint64_t)epr == 0 && !diag_env("LCMA_B2D") &&
               make_map_mn3d(&tb, Bop, dt, cols, rows, epr, p->BK, (uint32_t)((p->bn / p->cg) / p->BK), swz) ==
                   LCMA_OK;
         if (!b3d) rs = make_map(&tb, Bop, dt, cols, rows, epr, p->BK, swz);
@@ -809,12 +845,17 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     // MN-major 32-bit operands use the 128B_BASE32B layout (4-row swizzle atoms)
     g.b_layout_type = (dt == LCMA_TF32) ? 1 : 2;
     g.b_sbo = (dt == LCMA_TF32) ? 512 : 1024;
-    if (const char* v = std::getenv("LCMA_TF32_MN_LT")) g.b_layout_type = std::atoi(v);
-    if (const char* v = std::getenv("LCMA_TF32_MN_SBO")) g.b_sbo = std::atoi(v);
+    if (const char* v = diag_env("LCMA_TF32_MN_LT")) g.b_layout_type = std::atoi(v);
+    if (const char* v = diag_env("LCMA_TF32_MN_SBO")) g.b_sbo = std::atoi(v);
     g.tf32 = dt == LCMA_TF32;
     g.idesc = ptx::make_idesc(dt == LCMA_BF16 ? 1u : dt == LCMA_FP16 ? 0u : 2u, kBM * p->cg, p->bn,
                               b_mn ? 1u : 0u, 0u);
     g.W = p->ctas / p->cg; g.q = p->q; g.tail_c = p->tail_c; g.swz = p->swz;
+    g.n_whole = p->n_whole;
+    g.dyn = (p->dyn && sched && !pf) ? 1 : 0;
+    g.sched = sched;
+    g.pf_dist = p->pf_dist;
+    if (const char* v = diag_env("LCMA_PREFETCH")) g.pf_dist = std::max(0, std::atoi(v));
     g.epi_mode = H ? EPI_STORE_H : EPI_FUSED;
     g.out_type = (p->d.out_dtype == LCMA_FP32 || p->d.out_dtype == LCMA_TF32) ? OUT_FP32
                  : p->d.out_dtype == LCMA_BF16 ? OUT_BF16 : OUT_FP16;
@@ -824,18 +865,18 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     {
         const int ce = g.out_type == OUT_FP32 ? 4 : 2;
         g.c_v8 = ((reinterpret_cast<uintptr_t>(C) & 31) == 0 && (g.ldc * ce) % 32 == 0) ? 1 : 0;
-        if (std::getenv("LCMA_NO_V8")) g.c_v8 = 0;
-        g.c_cs = std::getenv("LCMA_C_CS") ? std::atoi(std::getenv("LCMA_C_CS")) : 0;
+        if (diag_env("LCMA_NO_V8")) g.c_v8 = 0;
+        g.c_cs = diag_env("LCMA_C_CS") ? std::atoi(diag_env("LCMA_C_CS")) : 0;
     }
-    if (const char* dbg = std::getenv("LCMA_DEBUG")) g.debug = std::atoi(dbg);
+    if (const char* dbg = diag_env("LCMA_DEBUG")) g.debug = std::atoi(dbg);
     // fused Combine H partials carry an L2 evict_last policy (measured: -1 %
     // at cfg2, -3..7 % at the cfg5 shard; profiles/r01b_l2_residency.txt)
     g.partial_hint = 1;
-    if (const char* ph = std::getenv("LCMA_PARTIAL_HINT")) g.partial_hint = std::atoi(ph);
-    if (const char* oh = std::getenv("LCMA_OPERAND_HINT")) g.operand_hint = std::atoi(oh);
-    if (const char* sw = std::getenv("LCMA_SWZ")) g.swz = std::max(1, std::atoi(sw));
-    if (std::getenv("LCMA_STATS")) g.stats = lcma_debug_stats_buffer();
-    if (std::getenv("LCMA_TIMELINE")) g.tl = lcma_debug_timeline_buffer();
+    if (const char* ph = diag_env("LCMA_PARTIAL_HINT")) g.partial_hint = std::atoi(ph);
+    if (const char* oh = diag_env("LCMA_OPERAND_HINT")) g.operand_hint = std::atoi(oh);
+    if (const char* sw = diag_env("LCMA_SWZ")) g.swz = std::max(1, std::atoi(sw));
+    if (diag_env("LCMA_STATS")) g.stats = lcma_debug_stats_buffer();
+    if (diag_env("LCMA_TIMELINE")) g.tl = lcma_debug_timeline_buffer();
     const int mn = S.m * S.n;
     if (S.R > kMaxR || mn > kMaxMN) return fail(LCMA_ERR_NOT_SUPPORTED, "scheme too large for the fused kernel");
     for (int r = 0; r < S.R; ++r) {
@@ -852,7 +893,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     // product order inside a group + partial homes (fused Combine H, whole
     // groups): the two C_ij slots with the most partial updates live on chip
     // (epilogue registers, shared memory), the others in L2 workspace slots
-    const bool use_order = !std::getenv("LCMA_ORDER") || std::atoi(std::getenv("LCMA_ORDER")) != 0;
+    const bool use_order = !diag_env("LCMA_ORDER") || std::atoi(diag_env("LCMA_ORDER")) != 0;
     for (int ij = 0; ij < kMaxMN; ++ij) g.home[ij] = 0;
     if (use_order && !classical) {
         const ProductOrder& po = scheme_product_order(p->scheme_id);
@@ -860,8 +901,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         // slot -> home
         const int ns = po.nslot;
         const std::vector<int>& by_use = po.by_use;
-        const bool use_reg = regh && !(std::getenv("LCMA_REG_PARTIAL") && std::atoi(std::getenv("LCMA_REG_PARTIAL")) == 0);
-        const bool use_smem = !H && !pf && !(std::getenv("LCMA_SMEM_PARTIAL") && std::atoi(std::getenv("LCMA_SMEM_PARTIAL")) == 0);
+        const bool use_reg = regh && !(diag_env("LCMA_REG_PARTIAL") && std::atoi(diag_env("LCMA_REG_PARTIAL")) == 0);
+        const bool use_smem = !H && !pf && !(diag_env("LCMA_SMEM_PARTIAL") && std::atoi(diag_env("LCMA_SMEM_PARTIAL")) == 0);
         std::vector<int> slot_home(ns, 0);
         int nl2 = 0, k0 = 0;
         if (use_reg && k0 < ns) slot_home[by_use[k0++]] = HOME_REG;
@@ -878,10 +919,10 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         g.nslot = mn;
     }
     g.serpentine = 0;
-    if (const char* v = std::getenv("LCMA_SERPENTINE")) g.serpentine = std::atoi(v);
+    if (const char* v = diag_env("LCMA_SERPENTINE")) g.serpentine = std::atoi(v);
     g.discard = 1;
-    if (const char* dc = std::getenv("LCMA_DISCARD")) g.discard = std::atoi(dc);
-    if (const char* pn = std::getenv("LCMA_PACE_NS")) g.pace_ns = std::atoi(pn);
+    if (const char* dc = diag_env("LCMA_DISCARD")) g.discard = std::atoi(dc);
+    if (const char* pn = diag_env("LCMA_PACE_NS")) g.pace_ns = std::atoi(pn);
     if (t_ev_start) cudaEventRecord(t_ev_start, st);
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));
@@ -899,8 +940,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     }
     // optional: keep the whole-group partial slots L2-resident (access-policy
     // window over [P, P + nslot*ctas tiles), persisting)
-    if (P && g.epi_mode == EPI_FUSED && std::getenv("LCMA_L2PERSIST")) {
-        size_t want = (size_t)std::atoll(std::getenv("LCMA_L2PERSIST")) << 20;
+    if (P && g.epi_mode == EPI_FUSED && diag_env("LCMA_L2PERSIST")) {
+        size_t want = (size_t)std::atoll(diag_env("LCMA_L2PERSIST")) << 20;
         int maxp = 0, dev0 = 0;
         cudaGetDevice(&dev0);
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev0);
@@ -1035,7 +1076,7 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
             if (p->d.out_dtype != LCMA_FP32) return fail(LCMA_ERR_NOT_SUPPORTED, "fp32 output only");
             return launch_simt(p, (const float*)A, (const float*)B, (float*)C, st);
         }
-        return launch_umma(p, A, B, C, nullptr, nullptr, nullptr, st);
+        return launch_umma(p, A, B, C, nullptr, nullptr, reinterpret_cast<int*>(w + p->off_sched), nullptr, st);
     }
     void* At = w + p->off_At;
     const void* Bt = Bt_user;
@@ -1051,7 +1092,7 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
         pf = 1;
         const Scheme& S = p->sch;
         bool two = p->d.b_layout == 1 && !Bt_user && p->d.N == (int64_t)S.n * p->Nb &&
-                   p->d.K == (int64_t)S.k * p->Kb && !std::getenv("LCMA_PF_A_ONLY");
+                   p->d.K == (int64_t)S.k * p->Kb && !diag_env("LCMA_PF_A_ONLY");
         for (int r = 0; r < S.R && two; ++r) {
             int nz = 0;
             for (int a = 0; a < S.k; ++a)
@@ -1083,13 +1124,14 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
         const size_t h_slice = (size_t)(B0.m * p->Mb) * (B0.n * p->Nb);
         float* Pi = reinterpret_cast<float*>(w + p->off_inner + in->off_P);
         int* Fi = reinterpret_cast<int*>(w + p->off_inner + in->off_flags);
+        int* Si = reinterpret_cast<int*>(w + p->off_inner + in->off_sched);
         // the measurement events bracket all inner GEMMs together
         cudaEvent_t ev0 = t_ev_start, ev1 = t_ev_end;
         t_ev_start = t_ev_end = nullptr;
         if (ev0) cudaEventRecord(ev0, st);
         for (int q = 0; q < B0.R && rs == LCMA_OK; ++q)
             rs = launch_umma(in, static_cast<const uint8_t*>(At) + q * a_slice,
-                             static_cast<const uint8_t*>(Bt) + q * b_slice, H + q * h_slice, Pi, Fi, nullptr, st);
+                             static_cast<const uint8_t*>(Bt) + q * b_slice, H + q * h_slice, Pi, Fi, Si, nullptr, st);
         if (ev1) cudaEventRecord(ev1, st);
         t_ev_start = ev0;
         t_ev_end = ev1;
@@ -1098,15 +1140,16 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
     }
     if (p->variant == LCMA_VARIANT_UNFUSED) {
         float* H = reinterpret_cast<float*>(w + p->off_H);
-        rs = launch_umma(p, At, Bt, C, nullptr, nullptr, H, st);
+        rs = launch_umma(p, At, Bt, C, nullptr, nullptr, reinterpret_cast<int*>(w + p->off_sched), H, st);
         if (rs != LCMA_OK) return rs;
         return launch_combine_h(p, H, C, st);
     }
     if (p->variant == LCMA_VARIANT_PRODUCER)   // Combine A (and B) inside the GEMM's producer path
         return launch_umma(p, A, pf == 2 ? B : Bt, C, reinterpret_cast<float*>(w + p->off_P),
-                           reinterpret_cast<int*>(w + p->off_flags), nullptr, st, pf);
+                           reinterpret_cast<int*>(w + p->off_flags), nullptr, nullptr, st, pf);
     return launch_umma(p, At, Bt, C, reinterpret_cast<float*>(w + p->off_P),
-                       reinterpret_cast<int*>(w + p->off_flags), nullptr, st);
+                       reinterpret_cast<int*>(w + p->off_flags), reinterpret_cast<int*>(w + p->off_sched), nullptr,
+                       st);
 }
 
 }  // namespace

@@ -52,6 +52,8 @@ constexpr int kEpiWarps = 8;
 constexpr int kMaxR = 128;
 constexpr int kMaxMN = 32;
 constexpr int kTlMax = 512;       // timeline entries per CTA
+constexpr int kSchedDepth = 8;    // dynamic schedule: units published ahead of their consumers
+constexpr int kBarBytes = 512;    // mbarriers, TMEM slot and schedule ring
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -83,9 +85,9 @@ struct Cfg {
     static constexpr int kMaxStages = NP ? LCMA_MAX_STAGES_NP : LCMA_MAX_STAGES;
     // as many stages as fit in 227 KB (minus the partial, alignment slack and
     // barriers), <= LCMA_MAX_STAGES
-    static constexpr int kFree = 232448 - 1024 - 256 - kPartialSmem;
+    static constexpr int kFree = 232448 - 1024 - kBarBytes - kPartialSmem;
     static constexpr int kStages = (kFree / kStageBytes) > kMaxStages ? kMaxStages : (kFree / kStageBytes);
-    static constexpr int kSmemBytes = kStages * kStageBytes + kPartialSmem + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kPartialSmem + 1024 /*align*/ + kBarBytes;
 };
 
 // The 256-column pair kernel without a register home is only launched for
@@ -120,6 +122,11 @@ struct GemmParams {
     int q;                 // lockstep rounds of whole groups
     int tail_c;            // tile capacity per unit in the split tail
     int swz;               // raster band height (tiles) for group -> (x, z)
+    int n_whole;           // groups processed whole before the split tail (static: q * W, <= G)
+    int dyn;               // 1: whole groups handed out at run time in raster order (ticket
+                           //    counter `sched`, SchedRing broadcast to every role of the pair)
+    int* sched;            // dyn: ticket counter (workspace, zero between launches)
+    int pf_dist;           // >0: L2 prefetch of the operand tiles this many k-blocks ahead
     // epilogue
     int epi_mode;
     int out_type;
@@ -169,23 +176,103 @@ struct Unit {
     int rev;             // whole group of an odd lockstep round: products in reverse order
 };
 
+// Shared-memory ring through which the pair leader's producer (the
+// scheduler) hands dynamically drawn whole groups to every other role of the
+// pair: slot[k % D] = group of the k-th dynamic unit (-1: the dynamic phase
+// is over), full[] armed by the scheduler (locally, and remotely in the peer
+// CTA), empty[] (leader only) counts the consumers that have read the slot.
+struct SchedRing {
+    int* slot;
+    uint64_t* full;
+    uint64_t* empty;
+};
+enum SchedRole : int { SR_SCHED = 0, SR_LOCAL = 1, SR_PEER = 2 };
+
 // Enumerates the units of work-unit slot `w` in processing order.  Every role
 // of the CTA (producer, MMA, epilogue) and both CTAs of a pair walk the same
-// sequence.
+// sequence.  Static mode (dyn = 0): lockstep rounds, group idx*W + w, then the
+// split tail.  Dynamic mode: the first n_whole groups are drawn from a global
+// ticket counter in raster order by the leader's producer and broadcast via
+// the SchedRing (so the groups in flight always form a compact window of the
+// raster, however far the pairs drift apart), then the same static tail.
 struct UnitIter {
     const GemmParams& p;
     int w;
-    int idx;             // lockstep round index, then tail
+    int idx;             // lockstep round index (static), then tail
     int t, t_end;        // tail tile cursor (G * R < 2^31)
-    __device__ UnitIter(const GemmParams& p_, int w_) : p(p_), w(w_), idx(0) {
-        int Tt = (p.G - p.q * p.W) * p.R;
+    SchedRing ring;
+    int role;            // SchedRole (dynamic mode)
+    int k;               // dynamic units consumed / published so far
+    bool dyn_live;       // dynamic phase not over yet
+    uint32_t leader_empty0;   // SR_PEER: shared::cluster address of the leader's empty[0]
+    uint32_t peer_slot0, peer_full0;   // SR_SCHED with a peer: its slot[0] / full[0]
+    __device__ UnitIter(const GemmParams& p_, int w_, SchedRing ring_ = SchedRing{nullptr, nullptr, nullptr},
+                        int role_ = SR_LOCAL, int cg = 1)
+        : p(p_), w(w_), idx(0), ring(ring_), role(role_), k(0) {
+        int Tt = (p.G - p.n_whole) * p.R;
         if (Tt < 0) Tt = 0;
         t = w * p.tail_c;
         t_end = t + p.tail_c;
         if (t_end > Tt) t_end = Tt;
         if (t > Tt) t = Tt;
+        dyn_live = p.dyn != 0 && ring.slot != nullptr;   // (the PF combine warps: static only)
+        if (dyn_live) idx = p.q;          // no static rounds
+        leader_empty0 = peer_slot0 = peer_full0 = 0;
+        if (dyn_live && cg == 2) {
+            if (role == SR_PEER) leader_empty0 = ptx::mapa_shared(ptx::smem_u32(ring.empty), 0);
+            if (role == SR_SCHED) {
+                peer_slot0 = ptx::mapa_shared(ptx::smem_u32(ring.slot), 1);
+                peer_full0 = ptx::mapa_shared(ptx::smem_u32(ring.full), 1);
+            }
+        }
     }
-    __device__ bool next(Unit& u) {
+    // next dynamic group (SR_SCHED: draw + publish; others: read); -1 = over.
+    // Warps call this with all lanes; lane 0 (or the single producer lane)
+    // does the arrivals.
+    __device__ int dyn_next(bool single_thread) {
+        const int s = k % kSchedDepth;
+        const uint32_t ph = (uint32_t)(k / kSchedDepth) & 1u;
+        int g;
+        if (role == SR_SCHED) {
+            ptx::mbar_wait(&ring.empty[s], ph ^ 1u);
+            const int W = (int)(gridDim.x) / (peer_slot0 ? 2 : 1);
+            const int tk = atomicAdd(p.sched, 1);
+            g = tk < p.n_whole ? tk : -1;
+            // every unit draws exactly one failing ticket; the last one drawn
+            // (n_whole + W - 1) resets the counter for the next launch
+            if (tk == p.n_whole + W - 1) atomicExch(p.sched, 0);
+            ring.slot[s] = g;
+            if (peer_slot0) {
+                ptx::st_shared_cluster_u32(peer_slot0 + 4u * s, (uint32_t)g);
+                ptx::mbar_arrive_cluster(peer_full0 + 8u * s);
+            }
+            ptx::mbar_arrive(&ring.full[s]);
+        } else {
+            if (role == SR_PEER) ptx::mbar_wait_cluster(&ring.full[s], ph);
+            else ptx::mbar_wait(&ring.full[s], ph);
+            g = *reinterpret_cast<volatile int*>(&ring.slot[s]);
+            if (!single_thread) __syncwarp();
+            if (single_thread || ptx::lane_id() == 0) {
+                if (role == SR_PEER) ptx::mbar_arrive_cluster(leader_empty0 + 8u * s);
+                else ptx::mbar_arrive(&ring.empty[s]);
+            }
+        }
+        ++k;
+        return g;
+    }
+    __device__ bool next(Unit& u, bool single_thread = false) {
+        if (dyn_live) {
+            const int g = dyn_next(single_thread);
+            if (g >= 0) {
+                u.g = g;
+                u.r0 = 0;
+                u.r1 = p.R;
+                u.role = ROLE_WHOLE;
+                u.rev = 0;
+                return true;
+            }
+            dyn_live = false;
+        }
         if (idx < p.q) {
             u.g = idx * p.W + w;
             if (u.g >= p.G) return false;      // schedule 3: last round of whole groups
@@ -205,7 +292,7 @@ struct UnitIter {
         int stop = (gl + 1) * p.R;
         if (stop > t_end) stop = t_end;
         int r1 = (int)(stop - gl * p.R);
-        u.g = p.q * p.W + (int)gl;
+        u.g = p.n_whole + (int)gl;
         u.r0 = r0;
         u.r1 = r1;
         u.role = (r0 == 0 && r1 == p.R) ? ROLE_WHOLE : (r0 == 0 ? ROLE_OWNER : ROLE_CONTRIB);
@@ -406,6 +493,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty_bar = tfull_bar + 2;        // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
     uint64_t* ld_bar = tempty_bar + 4;           // PF: [kStages] own A tiles landed (local)
+    uint64_t* sched_full = ld_bar + kStages;     // [kSchedDepth] dynamic schedule ring
+    uint64_t* sched_empty = sched_full + kSchedDepth;
+    int* sched_slot = reinterpret_cast<int*>(sched_empty + kSchedDepth);
+    const SchedRing ring{sched_slot, sched_full, sched_empty};
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -431,6 +522,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull_bar[a], 1);
             ptx::mbar_init(&tempty_bar[a], kEpiWarps * CG);
+        }
+        // schedule ring consumers of the leader's empty[]: MMA warp + epilogue
+        // warps (+ the peer's producer and epilogue warps)
+        for (int d = 0; d < kSchedDepth; ++d) {
+            ptx::mbar_init(&sched_full[d], 1);
+            ptx::mbar_init(&sched_empty[d], CG == 2 ? 2 + 2 * kEpiWarps : 1 + kEpiWarps);
         }
         ptx::fence_mbar_init();
     }
@@ -467,16 +564,43 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t opol = oh == 2 || oh == 3 ? ptx::policy_evict_last() : ptx::policy_evict_first();
             const uint64_t opol_b = oh == 2 || oh == 4 ? ptx::policy_evict_last() : ptx::policy_evict_first();
             const bool ohint = oh != 0;
-            UnitIter it(p, w);
-            Unit u;
-            while (it.next(u)) {
+            UnitIter it(p, w, ring, leader ? SR_SCHED : SR_PEER, CG);
+            // one unit of lookahead (the L2 prefetch may reach into it)
+            Unit u, un;
+            bool has_u = it.next(u, true);
+            bool has_un = has_u && it.next(un, true);
+            while (has_u) {
                 int x, z;
                 group_xz(p, u.g, x, z);
+                int xn = 0, zn = 0;
+                if (has_un) group_xz(p, un.g, xn, zn);
+                const int len_u = (u.r1 - u.r0) * p.nK;
                 for (int t = u.r0; t < u.r1; ++t) {
                     const int r = product_at(p, u, t);
                     const int a_row = r * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
                     const int b_col0 = z * BN + (int)rank * C_::kBNc;
                     for (int kb = 0; kb < p.nK; ++kb) {
+                        if (p.pf_dist > 0 && !PF) {
+                            // L2 prefetch of this CTA's tiles pf_dist k-blocks ahead in the
+                            // unit sequence (across product and unit boundaries)
+                            int pos = (t - u.r0) * p.nK + kb + p.pf_dist;
+                            const Unit* tu = &u;
+                            int tx = x, tz = z;
+                            if (pos >= len_u) {
+                                pos -= len_u;
+                                tu = (has_un && pos < (un.r1 - un.r0) * p.nK) ? &un : nullptr;
+                                tx = xn; tz = zn;
+                            }
+                            if (tu) {
+                                const int tq = pos / p.nK;
+                                const int pr = product_at(p, *tu, tu->r0 + tq);
+                                const int pk = (pos - tq * p.nK) * p.BK;
+                                ptx::tma_prefetch_2d(&tmap_a, pk, pr * p.a_rows_per_r + tx * C_::kTileM + (int)rank * kBM);
+                                const int pb0 = tz * BN + (int)rank * C_::kBNc;
+                                if (!p.b_mn_major) ptx::tma_prefetch_2d(&tmap_b, pk, pr * p.b_rows_per_r + pb0);
+                                else if (p.b_3d) ptx::tma_prefetch_3d(&tmap_b, 0, pr * p.b_rows_per_r + pk, pb0 / p.BK);
+                            }
+                        }
                         timed_wait(&empty_bar[stage], phase ^ 1, st_empty);
                         uint8_t* sa = smem + stage * C_::kStageBytes;
                         uint8_t* sb = sa + C_::kABytes;
@@ -566,6 +690,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
                 }
+                u = un;
+                has_u = has_un;
+                if (has_u) has_un = it.next(un, true);
             }
             if (p.stats) p.stats[blockIdx.x * 8 + 0] = w_empty;
         }
@@ -595,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t acc_phase = 0;
             unsigned long long w_tempty = 0, w_full = 0;
             const long long t_start = clock64();
-            UnitIter it(p, w);
+            UnitIter it(p, w, ring, SR_LOCAL, CG);
             Unit u;
             int tli = 0;
             while (it.next(u)) {
@@ -741,7 +868,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kPregCols = REGH ? BN / 2 : 1;
         float preg[kPregCols];
         int tl_i = 0;             // timeline product index (diagnostics)
-        UnitIter it(p, w);
+        UnitIter it(p, w, ring, leader ? SR_LOCAL : SR_PEER, CG);
         Unit u;
         while (it.next(u)) {
             int x, z;
@@ -896,6 +1023,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     if (!first && p.discard) {
                                         __syncwarp();      // the 8 lanes sharing a line have read it
                                         if ((row & 7) == 0) discard_lines(pt, row, c4, 8);
+                                        // a discard is a weak write of the whole line: order it
+                                        // before any lane's next store to the same home (a first
+                                        // contribution of this product may take it over)
+                                        __syncwarp();
                                     }
                                 } else if (first) {
 #pragma unroll
@@ -948,7 +1079,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 continue;
             }
             // owner: the other segments live on work units w+1 .. last (same rank)
-            const long long Tt_base = (long long)(u.g - p.q * p.W) * p.R;   // tail-local first tile
+            const long long Tt_base = (long long)(u.g - p.n_whole) * p.R;   // tail-local first tile
             const int last_w = (int)((Tt_base + p.R - 1) / p.tail_c);
             if (ew == 0 && lane == 0) {
                 for (int v = w + 1; v <= last_w; ++v) {

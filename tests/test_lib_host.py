@@ -105,7 +105,9 @@ def test_plan_extents_and_workspace():
     p2 = L.Plan(1000, 1048, 520, algo="laderman")
     i2 = p2.info
     assert 3 * i2["Mb"] >= 1000 and 3 * i2["Nb"] >= 1048 and 3 * i2["Kb"] >= 520
-    assert L.Plan(256, 256, 256, algo="classical").workspace_bytes == 0
+    # classical: only the dynamic schedule's ticket counter (256-byte region)
+    assert L.Plan(256, 256, 256, algo="classical").workspace_bytes == 256
+    assert L.Plan(256, 256, 256, algo="classical", schedule=4).workspace_bytes == 256
 
 
 def _flatten(plan):

@@ -203,3 +203,74 @@ def test_metrics_detect_sign_flip_block():
     bad[:32, :24] *= -1
     assert O.eps_rel(bad, C) > 0.3
     assert O.freivalds(bad, A, B) > 1e-3
+
+
+# ------------------------------------------------------------- metric pins
+def _golden_metrics():
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "metrics_2x2.txt")
+    rows = []
+    for ln in open(path):
+        if ln.strip() and not ln.startswith("#"):
+            f = ln.split()
+            rows.append((f[0], np.array([float(v) for v in f[1:5]]).reshape(2, 2), float(f[5]), float(f[6])))
+    return rows
+
+
+def test_metrics_hand_computed():
+    # tests/golden/metrics_2x2.txt: eps_norm / eps_rel on the S:175 example,
+    # hand-computed.  A squared norm, ||A B|| as the denominator, or a missing
+    # factor in ||A||_F ||B||_F changes these values.
+    A = np.array([[1.0, 2.0], [3.0, 4.0]])
+    B = np.array([[5.0, 6.0], [7.0, 8.0]])
+    Cref = O.gemm_f64(A, B)
+    for name, C, en, er in _golden_metrics():
+        assert O.eps_norm(C, Cref, A, B) == pytest.approx(en, rel=1e-8), name
+        assert O.eps_rel(C, Cref) == pytest.approx(er, rel=1e-8), name
+
+
+def test_metrics_scaling_laws():
+    # eps_norm is invariant under C, Cref -> a*C, a*Cref with A -> a*A, and
+    # scales as 1/(ab) when only A, B are scaled by a, b (the error fixed)
+    rng = np.random.default_rng(3)
+    A, B = rng.uniform(-1, 1, (9, 5)), rng.uniform(-1, 1, (5, 7))
+    Cref = A @ B
+    C = Cref + rng.uniform(-1e-3, 1e-3, Cref.shape)
+    e = O.eps_norm(C, Cref, A, B)
+    assert O.eps_norm(3 * C, 3 * Cref, 3 * A, B) == pytest.approx(e, rel=1e-12)
+    assert O.eps_norm(C, Cref, 2 * A, 5 * B) == pytest.approx(e / 10, rel=1e-12)
+    assert O.eps_rel(4 * C, 4 * Cref) == pytest.approx(O.eps_rel(C, Cref), rel=1e-12)
+
+
+# ----------------------------------------------------------- roofline pins
+def test_roofline_rows_hand_computed():
+    # S:439-445 roofline rows at AI = 100 (square N = 1.5*AI = 150), Strassen
+    # <2,2,2;7> (nnz 12/12/12), profile FLOPS_x = FLOPS_+ = 10, beta = 1, so
+    # thr/beta = 10.  By hand from the Table, Mq = Kq = Nq = 75:
+    #  A: flops 5*75^2 = 28125, mem 150^2 + 7*75^2 = 61875 -> AI .45 < 10 -> t 61875
+    #  B: the same, t 61875
+    #  GEMM: flops 2*7*75^3 = 5906250, mem 7*(2*75^2) + 150^2 = 101250 (fused)
+    #        -> AI 58.3 > 10 -> t = 590625
+    #  H: flops 8*75^2 = 45000, mem 150^2 = 22500 -> AI 2 < 10 -> t 22500
+    #  total 736875 -> effective 2*150^3 / 736875 = 10800/1179
+    #  unfused: GEMM mem + 7*75^2 (still compute), H mem 22500 + 39375 = 61875
+    #  -> total 776250 -> effective 200/23; classical 2*150^3/10 -> effective 10.
+    hw = O.Profile(10.0, 10.0, 1.0)
+    rows = {(a, n): v for a, n, v in O.roofline_table([O.strassen()], hw, [100])}
+    assert rows[(100, "classical")] == pytest.approx(10.0, rel=1e-12)
+    assert rows[(100, "strassen-2x2x2-r7")] == pytest.approx(10800 / 1179, rel=1e-12)
+    rows_u = {(a, n): v for a, n, v in O.roofline_table([O.strassen()], hw, [100], fused=False)}
+    assert rows_u[(100, "strassen-2x2x2-r7")] == pytest.approx(200 / 23, rel=1e-12)
+
+
+def test_roofline_compute_ceiling():
+    # beta, FLOPS_+ -> infinity: every stage but the GEMM vanishes and the LCMA
+    # row reaches its effective ceiling FLOPS_x * mnk / R exactly
+    hw = O.Profile(1.0, 1e30, 1e30)
+    cat = [O.strassen(), O.strassen2(), O.laderman()]
+    # AI = 576 -> N = 864, divisible by 2, 3 and 4 (no padding)
+    rows = {n: v for a, n, v in O.roofline_table(cat, hw, [576])}
+    assert rows["classical"] == pytest.approx(1.0, rel=1e-12)
+    assert rows[O.strassen().name] == pytest.approx(8 / 7, rel=1e-9)
+    assert rows[O.strassen2().name] == pytest.approx(64 / 49, rel=1e-9)
+    assert rows[O.laderman().name] == pytest.approx(27 / 23, rel=1e-9)

@@ -147,3 +147,27 @@ def test_precision_direction_downcast_h():
 def test_zero_inputs():
     s = O.strassen()
     assert not O.lcma_f64(np.zeros((5, 6)), np.zeros((6, 7)), s).C.any()
+
+
+@pytest.mark.parametrize("scheme", ["strassen", "laderman", "strassen2"])
+def test_lcma_rows_matches_full_evaluator(scheme):
+    # the row-restricted Algorithm 1 (sampled full-size checks) equals the
+    # whole evaluator's rows: exactly on integer-valued inputs (ragged shape,
+    # GPU-like padded extents), and within fp64 summation order on floats with
+    # the bf16 rounding points (C rounded once: at most one bf16 ulp apart)
+    s = getattr(O, scheme)()
+    rng = np.random.default_rng(21)
+    M, N, K = 70, 52, 38
+    ext = (-(-M // s.m) + 3, -(-K // s.k) + 1, -(-N // s.n) + 2)
+    rows = np.array([0, 1, ext[0] - 1, ext[0], M - 1, 33])
+    Ai = rng.integers(-3, 4, (M, K)).astype(np.float64)
+    Bi = rng.integers(-3, 4, (K, N)).astype(np.float64)
+    got = O.lcma_rows_f64(Ai, Bi, s, rows, extents=ext)
+    assert np.array_equal(got, O.gemm_f64(Ai, Bi)[rows])
+    assert np.array_equal(got, O.lcma_f64(Ai, Bi, s, extents=ext).C[rows])
+    A = rng.uniform(-1, 1, (M, K))
+    B = rng.uniform(-1, 1, (K, N))
+    full = O.lcma_f64(A, B, s, extents=ext, fmt_in="bf16", fmt_out="bf16").C[rows]
+    got = O.lcma_rows_f64(A, B, s, rows, extents=ext, fmt_in="bf16", fmt_out="bf16")
+    assert np.all(np.abs(got - full) <= 2.0 ** -7 * np.abs(full) + 1e-300)
+    assert np.mean(got == full) > 0.95

@@ -8,6 +8,7 @@ usage: python tools/ablation.py [M N K] [--static]   -> JSON on stdout
        ABL_ONE=<name> python tools/ablation.py ...   -> one launch (for ncu)
 """
 import json, os, statistics, sys
+os.environ.setdefault("LCMA_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)).split("/tools")[0], "paper_2605_06057_b200", "liblcma_diag.so"))  # env knobs: -DLCMA_DIAG build
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2605_06057_b200 as L

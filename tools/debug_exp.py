@@ -1,6 +1,7 @@
 """Classical kernel time with epilogue parts disabled (LCMA_DEBUG bits:
 1 = no global traffic, 2 = no TMEM loads)."""
 import os, sys
+os.environ.setdefault("LCMA_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)).split("/tools")[0], "paper_2605_06057_b200", "liblcma_diag.so"))  # env knobs: -DLCMA_DIAG build
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2605_06057_b200 as L

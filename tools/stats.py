@@ -1,5 +1,6 @@
 """Per-role wait-cycle breakdown of the tcgen05 kernel (LCMA_STATS=1)."""
 import sys, os, ctypes
+os.environ.setdefault("LCMA_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)).split("/tools")[0], "paper_2605_06057_b200", "liblcma_diag.so"))  # env knobs: -DLCMA_DIAG build
 os.environ["LCMA_STATS"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

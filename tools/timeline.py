@@ -2,6 +2,7 @@
 warp waits for the epilogue to release an accumulator slot, by product
 position inside the group.  usage: python tools/timeline.py [algo] [M N K]"""
 import ctypes, os, sys
+os.environ.setdefault("LCMA_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)).split("/tools")[0], "paper_2605_06057_b200", "liblcma_diag.so"))  # env knobs: -DLCMA_DIAG build
 os.environ["LCMA_TIMELINE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
