@@ -115,14 +115,14 @@ typedef struct {
     int32_t b_layout;         /* 0: B is K x N (paper), 1: B is N x K              */
     int32_t b_static;         /* 1: lcma_gemm_precombined will be used     */
     int32_t variant;          /* lcma_variant                                      */
-    int32_t schedule;         /* 0 auto = 1; 1 cache-aware: whole groups handed out
-                                 in raster order at run time (ticket counter in the
-                                 workspace, so the groups in flight stay a compact
-                                 window of the raster) + the split tail;
+    int32_t schedule;         /* 0 auto = 1; 1 = 4: cache-aware lockstep rounds
+                                 (group w + i*W to unit w) + split tail;
                                  2 paper's contiguous split-group order;
                                  3 whole groups only (group-parallel, no split);
-                                 4 static lockstep rounds (group w + i*W to unit w)
-                                   + split tail (round-1 schedule, ablation)       */
+                                 5 whole groups handed out in raster order at run
+                                   time (ticket counter in the workspace: the groups
+                                   in flight stay a compact window of the raster)
+                                   + the split tail                                */
     int32_t num_ctas;         /* 0 = one per SM                                    */
     const lcma_hw_profile* hw;/* NULL -> built-in B200 profile                     */
     int32_t decision_model;   /* algo AUTO: 0 = this build's B200-calibrated model
@@ -130,9 +130,8 @@ typedef struct {
                                  verbatim (as lcma_decide)              */
     /* tuning (0 = the measured default for the shape; results are identical
        for every value, only the time changes) */
-    int32_t prefetch_kblocks; /* L2 prefetch of operand tiles this many 64-element
-                                 k-blocks ahead of their TMA load; < 0: off        */
     int32_t raster_rows;      /* group raster: band height in tile rows            */
+    int32_t reserved;         /* must be 0                                         */
 } lcma_plan_desc;
 
 typedef struct {

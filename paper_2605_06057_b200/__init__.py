@@ -43,7 +43,7 @@ class PlanDesc(ctypes.Structure):
                 ("b_static", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("schedule", ctypes.c_int32), ("num_ctas", ctypes.c_int32),
                 ("hw", ctypes.POINTER(HwProfile)), ("decision_model", ctypes.c_int32),
-                ("prefetch_kblocks", ctypes.c_int32), ("raster_rows", ctypes.c_int32)]
+                ("raster_rows", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -143,7 +143,7 @@ class Plan:
 
     def __init__(self, M, N, K, dtype=BF16, algo="auto", out_dtype=None, b_layout=0,
                  variant="auto", b_static=False, schedule=0, num_ctas=0, scheme_id=0, hw=None,
-                 decision_model=0, prefetch_kblocks=0, raster_rows=0):
+                 decision_model=0, raster_rows=0):
         L = lib()
         if out_dtype is None:
             out_dtype = FP32 if dtype == TF32 else dtype
@@ -151,7 +151,7 @@ class Plan:
         d = PlanDesc(M, N, K, dtype, out_dtype, ALGO[algo] if isinstance(algo, str) else algo,
                      scheme_id, b_layout, int(b_static),
                      VARIANT[variant] if isinstance(variant, str) else variant,
-                     schedule, num_ctas, self._hw, decision_model, prefetch_kblocks, raster_rows)
+                     schedule, num_ctas, self._hw, decision_model, raster_rows, 0)
         h = ctypes.c_void_p()
         _check(L.lcma_plan_ex(ctypes.byref(d), ctypes.byref(h)))
         self._h = h

@@ -35,7 +35,7 @@ lcma_status fail(lcma_status st, const std::string& msg) {
 }
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
-constexpr int kDefaultPrefetch = 0;    // L2 prefetch distance when the desc says 0 (auto)
+
 int64_t roundup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -102,7 +102,7 @@ struct lcma_plan_s {
     int BK, e;
     int nX, nZ, G, nK;
     int ctas, cg, bn, q, tail_c, swz;
-    int n_whole, dyn, pf_dist;
+    int n_whole, dyn;
     size_t off_sched, off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
     size_t off_inner = 0;          // two-level: the inner plan's partial slots + flags
     lcma_plan_s* inner = nullptr;  // two-level: fused GEMM plan of the base scheme
@@ -148,11 +148,14 @@ void make_schedule(lcma_plan_s* p, int mode) {
         p->q = (int)cdiv(p->G, W);             // group-parallel only: whole groups, no split
     } else {
         p->q = p->G / W;                       // lockstep rounds (cache-aware)
-        // mode 1 (default): the whole groups are handed out at run time in
-        // raster order (the pairs drift apart by a round every ~50 rounds
-        // under a static assignment, which scatters the groups in flight over
-        // the raster: tools/r02/drift.py); mode 4: static rounds
-        p->dyn = mode == 4 ? 0 : 1;
+        // mode 5: the whole groups are handed out at run time in raster order
+        // (the pairs of the static assignment drift apart by about one round
+        // every 50 rounds, tools/r02/drift.py; the dynamic order keeps the
+        // groups in flight a compact window of the raster and halves the DRAM
+        // reads at the cfg5 shape, but measured no faster: within +-1 % at
+        // cfg2, -8..-16 % (classical) / -2..+9 % (Strassen) at cfg5,
+        // profiles/r02_schedule.txt), so the default (1 = 4) stays static
+        p->dyn = mode == 5 ? 1 : 0;
     }
     p->n_whole = (int)std::min<long long>((long long)p->q * W, p->G);
     // R == 1 (classical): nothing to split, every group is handed out whole
@@ -332,10 +335,9 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             return fail(LCMA_ERR_NOT_SUPPORTED, "problem too large for 32-bit tile coordinates");
         }
         p->G = p->nX * p->nZ;
-        make_schedule(p, (d.schedule >= 2 && d.schedule <= 4) ? d.schedule : 1);
+        make_schedule(p, (d.schedule >= 2 && d.schedule <= 5) ? d.schedule : 1);
         if (variant == LCMA_VARIANT_PRODUCER) p->dyn = 0;   // its combine warps walk the static schedule
-        // L2 prefetch distance (k-blocks): measured default
-        p->pf_dist = d.prefetch_kblocks < 0 ? 0 : d.prefetch_kblocks > 0 ? d.prefetch_kblocks : kDefaultPrefetch;
+
         if (variant == LCMA_VARIANT_PRODUCER &&
             (p->cg != 2 || p->bn != 256 || d.M != (int64_t)S.m * p->Mb || d.K != (int64_t)S.k * p->Kb)) {
             delete p;
@@ -635,11 +637,11 @@ lcma_status make_map_mn3d(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64
 unsigned long long* g_stats = nullptr;
 unsigned long long* lcma_debug_stats_buffer() {
     if (!g_stats) {
-        if (cudaMalloc(&g_stats, 1024 * 8 * sizeof(unsigned long long)) != cudaSuccess) {
+        if (cudaMalloc(&g_stats, 1024 * kStatsPerCta * sizeof(unsigned long long)) != cudaSuccess) {
             cudaGetLastError();
             g_stats = nullptr;
         } else {
-            cudaMemset(g_stats, 0, 1024 * 8 * sizeof(unsigned long long));
+            cudaMemset(g_stats, 0, 1024 * kStatsPerCta * sizeof(unsigned long long));
         }
     }
     return g_stats;
@@ -854,8 +856,13 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     g.n_whole = p->n_whole;
     g.dyn = (p->dyn && sched && !pf) ? 1 : 0;
     g.sched = sched;
-    g.pf_dist = p->pf_dist;
-    if (const char* v = diag_env("LCMA_PREFETCH")) g.pf_dist = std::max(0, std::atoi(v));
+    // product-boundary L2 prefetch: removes the first-k-block stall (MMA
+    // operand wait at k-block 0 of a product 2872 -> 270 cycles, classical
+    // cfg2) but the wait reappears later in the product: no faster (-0..-5 %),
+    // off by default (profiles/r02_schedule.txt)
+    g.pf = 0;
+    if (const char* v = diag_env("LCMA_PF")) g.pf = std::atoi(v);
+
     g.epi_mode = H ? EPI_STORE_H : EPI_FUSED;
     g.out_type = (p->d.out_dtype == LCMA_FP32 || p->d.out_dtype == LCMA_TF32) ? OUT_FP32
                  : p->d.out_dtype == LCMA_BF16 ? OUT_BF16 : OUT_FP16;

@@ -52,7 +52,10 @@ constexpr int kEpiWarps = 8;
 constexpr int kMaxR = 128;
 constexpr int kMaxMN = 32;
 constexpr int kTlMax = 512;       // timeline entries per CTA
+constexpr int kStatsPerCta = 16;  // diagnostics: wait counters per CTA (LCMA_STATS)
 constexpr int kSchedDepth = 8;    // dynamic schedule: units published ahead of their consumers
+constexpr int kPfLead = 8;        // product-boundary L2 prefetch: k-blocks ahead ...
+constexpr int kPfK = 4;           // ... of the next product's first kPfK k-blocks
 constexpr int kBarBytes = 512;    // mbarriers, TMEM slot and schedule ring
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -124,9 +127,9 @@ struct GemmParams {
     int swz;               // raster band height (tiles) for group -> (x, z)
     int n_whole;           // groups processed whole before the split tail (static: q * W, <= G)
     int dyn;               // 1: whole groups handed out at run time in raster order (ticket
-                           //    counter `sched`, SchedRing broadcast to every role of the pair)
+                           //    counter `sched`, broadcast to every role of the pair via a shared ring)
     int* sched;            // dyn: ticket counter (workspace, zero between launches)
-    int pf_dist;           // >0: L2 prefetch of the operand tiles this many k-blocks ahead
+    int pf;                // 1: L2 prefetch of each next product's first k-blocks (pair leader)
     // epilogue
     int epi_mode;
     int out_type;
@@ -178,14 +181,14 @@ struct Unit {
 
 // Shared-memory ring through which the pair leader's producer (the
 // scheduler) hands dynamically drawn whole groups to every other role of the
-// pair: slot[k % D] = group of the k-th dynamic unit (-1: the dynamic phase
-// is over), full[] armed by the scheduler (locally, and remotely in the peer
-// CTA), empty[] (leader only) counts the consumers that have read the slot.
-struct SchedRing {
-    int* slot;
-    uint64_t* full;
-    uint64_t* empty;
-};
+// pair.  One 32-bit shared address `ring` locates it (kept small: the
+// producer / MMA warps run with few registers): full[d] mbarriers at
+// ring + 8d (armed by the scheduler, locally and in the peer CTA), empty[d]
+// at ring + 8D + 8d (leader only: the consumers that have read slot d), and
+// slot[d] (int, group of the k-th dynamic unit with k % D == d; -1: the
+// dynamic phase is over) at ring + 16D + 4d.
+constexpr uint32_t kRingFull = 0, kRingEmpty = 8 * kSchedDepth, kRingSlot = 16 * kSchedDepth;
+constexpr int kRingBytes = 20 * kSchedDepth;
 enum SchedRole : int { SR_SCHED = 0, SR_LOCAL = 1, SR_PEER = 2 };
 
 // Enumerates the units of work-unit slot `w` in processing order.  Every role
@@ -193,75 +196,105 @@ enum SchedRole : int { SR_SCHED = 0, SR_LOCAL = 1, SR_PEER = 2 };
 // sequence.  Static mode (dyn = 0): lockstep rounds, group idx*W + w, then the
 // split tail.  Dynamic mode: the first n_whole groups are drawn from a global
 // ticket counter in raster order by the leader's producer and broadcast via
-// the SchedRing (so the groups in flight always form a compact window of the
+// the ring (so the groups in flight always form a compact window of the
 // raster, however far the pairs drift apart), then the same static tail.
 struct UnitIter {
     const GemmParams& p;
     int w;
     int idx;             // lockstep round index (static), then tail
     int t, t_end;        // tail tile cursor (G * R < 2^31)
-    SchedRing ring;
-    int role;            // SchedRole (dynamic mode)
     int k;               // dynamic units consumed / published so far
-    bool dyn_live;       // dynamic phase not over yet
-    uint32_t leader_empty0;   // SR_PEER: shared::cluster address of the leader's empty[0]
-    uint32_t peer_slot0, peer_full0;   // SR_SCHED with a peer: its slot[0] / full[0]
-    __device__ UnitIter(const GemmParams& p_, int w_, SchedRing ring_ = SchedRing{nullptr, nullptr, nullptr},
-                        int role_ = SR_LOCAL, int cg = 1)
-        : p(p_), w(w_), idx(0), ring(ring_), role(role_), k(0) {
+    uint32_t ring;       // shared address of the ring; 0: static schedule only
+    int role;            // SchedRole | (CG == 2 ? 4 : 0)
+    int pend;            // SR_SCHED: ticket drawn, not yet published (-1: none, -2: phase over)
+    int pub;             // SR_SCHED: ring slots published so far
+    __device__ UnitIter(const GemmParams& p_, int w_, uint32_t ring_ = 0u, int role_ = SR_LOCAL, int cg = 1)
+        : p(p_), w(w_), idx(0), k(0), ring(p_.dyn ? ring_ : 0u), role(role_ | (cg == 2 ? 4 : 0)), pend(-1),
+          pub(0) {
         int Tt = (p.G - p.n_whole) * p.R;
         if (Tt < 0) Tt = 0;
         t = w * p.tail_c;
         t_end = t + p.tail_c;
         if (t_end > Tt) t_end = Tt;
         if (t > Tt) t = Tt;
-        dyn_live = p.dyn != 0 && ring.slot != nullptr;   // (the PF combine warps: static only)
-        if (dyn_live) idx = p.q;          // no static rounds
-        leader_empty0 = peer_slot0 = peer_full0 = 0;
-        if (dyn_live && cg == 2) {
-            if (role == SR_PEER) leader_empty0 = ptx::mapa_shared(ptx::smem_u32(ring.empty), 0);
-            if (role == SR_SCHED) {
-                peer_slot0 = ptx::mapa_shared(ptx::smem_u32(ring.slot), 1);
-                peer_full0 = ptx::mapa_shared(ptx::smem_u32(ring.full), 1);
-            }
-        }
+        if (ring) idx = p.q;          // no static rounds
     }
     // next dynamic group (SR_SCHED: draw + publish; others: read); -1 = over.
     // Warps call this with all lanes; lane 0 (or the single producer lane)
     // does the arrivals.
+    // SR_SCHED: publish ring slot `pub` with ticket tk (group, or -1 once the
+    // whole-group phase is over); returns the group.
+    __device__ int publish(int tk) {
+        const uint32_t s = (uint32_t)(pub % kSchedDepth);
+        const uint32_t ph = (uint32_t)(pub / kSchedDepth) & 1u;
+        const bool pair = (role & 4) != 0;
+        ptx::mbar_wait_u32(ring + kRingEmpty + 8u * s, ph ^ 1u);
+        const int W = (int)gridDim.x / (pair ? 2 : 1);
+        const int g = tk < p.n_whole ? tk : -1;
+        // every unit draws exactly one failing ticket; the last one drawn
+        // (n_whole + W - 1) resets the counter for the next launch
+        if (tk == p.n_whole + W - 1) atomicExch(p.sched, 0);
+        ptx::st_shared_u32(ring + kRingSlot + 4u * s, (uint32_t)g);
+        if (pair) {
+            // the peer's copy: an asynchronous remote store completing 4 bytes
+            // of transaction on the peer's full[s] (armed by the relaxed
+            // expect_tx arrival): the scheduler never waits on the DSMEM trip
+            const uint32_t pbar = ptx::mapa_shared(ring + kRingFull + 8u * s, 1);
+            ptx::mbar_arrive_expect_tx_cluster_relaxed(pbar, 4u);
+            ptx::st_async_u32(ptx::mapa_shared(ring + kRingSlot + 4u * s, 1), (uint32_t)g, pbar);
+        }
+        ptx::mbar_arrive_u32(ring + kRingFull + 8u * s);
+        ++pub;
+        return g;
+    }
+    // SR_SCHED: publish the ring one unit ahead of its own position (the
+    // peer CTA and the consumers learn the next group early) and keep the
+    // ticket after that drawn (its L2 round trip overlaps a unit of loads).
+    // Called by the producer once the current unit's first loads are issued,
+    // so the handshake stays off the critical path.
+    __device__ void advance() {
+        if (!ring || (role & 3) != SR_SCHED) return;
+        while (pub <= k && pend != -2) {
+            const int tk = pend >= 0 ? pend : atomicAdd(p.sched, 1);
+            pend = -1;
+            if (publish(tk) < 0) pend = -2;
+        }
+        if (pend == -1) pend = atomicAdd(p.sched, 1);
+    }
+    // next dynamic group; -1 = over.  Warps call this with all lanes; lane 0
+    // (or the single producer lane) does the arrivals, relaxed: the slot value
+    // is already in a register.
     __device__ int dyn_next(bool single_thread) {
-        const int s = k % kSchedDepth;
+        const uint32_t s = (uint32_t)(k % kSchedDepth);
         const uint32_t ph = (uint32_t)(k / kSchedDepth) & 1u;
         int g;
-        if (role == SR_SCHED) {
-            ptx::mbar_wait(&ring.empty[s], ph ^ 1u);
-            const int W = (int)(gridDim.x) / (peer_slot0 ? 2 : 1);
-            const int tk = atomicAdd(p.sched, 1);
-            g = tk < p.n_whole ? tk : -1;
-            // every unit draws exactly one failing ticket; the last one drawn
-            // (n_whole + W - 1) resets the counter for the next launch
-            if (tk == p.n_whole + W - 1) atomicExch(p.sched, 0);
-            ring.slot[s] = g;
-            if (peer_slot0) {
-                ptx::st_shared_cluster_u32(peer_slot0 + 4u * s, (uint32_t)g);
-                ptx::mbar_arrive_cluster(peer_full0 + 8u * s);
+        if ((role & 3) == SR_SCHED) {
+            while (pub <= k && pend != -2) {        // (first unit, or advance() not called)
+                const int tk = pend >= 0 ? pend : atomicAdd(p.sched, 1);
+                pend = -1;
+                if (publish(tk) < 0) pend = -2;
             }
-            ptx::mbar_arrive(&ring.full[s]);
+            g = (int)ptx::ld_shared_u32(ring + kRingSlot + 4u * s);
         } else {
-            if (role == SR_PEER) ptx::mbar_wait_cluster(&ring.full[s], ph);
-            else ptx::mbar_wait(&ring.full[s], ph);
-            g = *reinterpret_cast<volatile int*>(&ring.slot[s]);
+            const bool peer = (role & 3) == SR_PEER;
+            if (peer) ptx::mbar_wait_cluster_u32(ring + kRingFull + 8u * s, ph);
+            else ptx::mbar_wait_u32(ring + kRingFull + 8u * s, ph);
+            g = (int)ptx::ld_shared_u32(ring + kRingSlot + 4u * s);
             if (!single_thread) __syncwarp();
             if (single_thread || ptx::lane_id() == 0) {
-                if (role == SR_PEER) ptx::mbar_arrive_cluster(leader_empty0 + 8u * s);
-                else ptx::mbar_arrive(&ring.empty[s]);
+                if (peer) ptx::mbar_arrive_cluster_relaxed(ptx::mapa_shared(ring + kRingEmpty + 8u * s, 0));
+                else ptx::mbar_arrive_relaxed_u32(ring + kRingEmpty + 8u * s);
             }
         }
         ++k;
         return g;
     }
+    // SR_SCHED: group of its next dynamic unit (published), else -1
+    __device__ int peek() const {
+        return (ring && pub > k) ? (int)ptx::ld_shared_u32(ring + kRingSlot + 4u * (uint32_t)(k % kSchedDepth)) : -1;
+    }
     __device__ bool next(Unit& u, bool single_thread = false) {
-        if (dyn_live) {
+        if (ring) {
             const int g = dyn_next(single_thread);
             if (g >= 0) {
                 u.g = g;
@@ -271,7 +304,7 @@ struct UnitIter {
                 u.rev = 0;
                 return true;
             }
-            dyn_live = false;
+            ring = 0u;          // dynamic phase over: the static tail follows
         }
         if (idx < p.q) {
             u.g = idx * p.W + w;
@@ -493,10 +526,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty_bar = tfull_bar + 2;        // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
     uint64_t* ld_bar = tempty_bar + 4;           // PF: [kStages] own A tiles landed (local)
-    uint64_t* sched_full = ld_bar + kStages;     // [kSchedDepth] dynamic schedule ring
+    uint64_t* sched_full = ld_bar + kStages;     // dynamic schedule ring (UnitIter)
     uint64_t* sched_empty = sched_full + kSchedDepth;
-    int* sched_slot = reinterpret_cast<int*>(sched_empty + kSchedDepth);
-    const SchedRing ring{sched_slot, sched_full, sched_empty};
+    const uint32_t ring = ptx::smem_u32(sched_full);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -504,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.stats && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.stats[blockIdx.x * 8 + 6] = t;
+        p.stats[blockIdx.x * kStatsPerCta + 6] = t;
     }
     const uint32_t rank = CG == 1 ? 0u : ptx::cluster_ctarank();
     const bool leader = rank == 0;
@@ -546,10 +578,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the branch with that budget.
 
     const int w = blockIdx.x / CG;           // work-unit slot (pair index for CG = 2)
+    // register split (128 * lo + 256 * hi <= 64 K): the register C_ij partial
+    // (REGH) needs 128 more registers per epilogue thread; without it the
+    // producer / MMA warps get room for the schedule state (no spills)
+    constexpr int kRegLo = REGH ? 40 : 88;
+    constexpr int kRegHi = REGH ? 232 : 208;
 
     if (warp == 0) {
         // ================================ TMA producer (both CTAs of a pair)
-        ptx::setmaxnreg_dec<40>();
+        ptx::setmaxnreg_dec<kRegLo>();
         if (ptx::elect_one()) {
             const int b_bytes_chunk = p.BK * 128;   // MN-major chunk: BK rows x 128 B
             const int n_chunks = C_::kBNc / p.BK;   // MN-major: 128-byte column chunks per CTA
@@ -565,40 +602,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t opol_b = oh == 2 || oh == 4 ? ptx::policy_evict_last() : ptx::policy_evict_first();
             const bool ohint = oh != 0;
             UnitIter it(p, w, ring, leader ? SR_SCHED : SR_PEER, CG);
-            // one unit of lookahead (the L2 prefetch may reach into it)
-            Unit u, un;
-            bool has_u = it.next(u, true);
-            bool has_un = has_u && it.next(un, true);
-            while (has_u) {
+            Unit u;
+            const int pf_at = p.nK > kPfLead ? p.nK - kPfLead : 0;
+            while (it.next(u, true)) {
                 int x, z;
                 group_xz(p, u.g, x, z);
-                int xn = 0, zn = 0;
-                if (has_un) group_xz(p, un.g, xn, zn);
-                const int len_u = (u.r1 - u.r0) * p.nK;
                 for (int t = u.r0; t < u.r1; ++t) {
                     const int r = product_at(p, u, t);
                     const int a_row = r * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
                     const int b_col0 = z * BN + (int)rank * C_::kBNc;
                     for (int kb = 0; kb < p.nK; ++kb) {
-                        if (p.pf_dist > 0 && !PF) {
-                            // L2 prefetch of this CTA's tiles pf_dist k-blocks ahead in the
-                            // unit sequence (across product and unit boundaries)
-                            int pos = (t - u.r0) * p.nK + kb + p.pf_dist;
-                            const Unit* tu = &u;
-                            int tx = x, tz = z;
-                            if (pos >= len_u) {
-                                pos -= len_u;
-                                tu = (has_un && pos < (un.r1 - un.r0) * p.nK) ? &un : nullptr;
-                                tx = xn; tz = zn;
+                        if (p.pf && leader && kb == pf_at) {
+                            // L2 prefetch of the first k-blocks of the next product (its
+                            // panels are new: their first loads would miss L2), for both
+                            // CTAs of the pair, kPfLead k-blocks before they are needed
+                            int nr = -1, nx = x, nz = z;
+                            if (t + 1 < u.r1) {
+                                nr = product_at(p, u, t + 1);
+                            } else {
+                                const int ng = it.peek();
+                                if (ng >= 0) { nr = p.rperm[0]; group_xz(p, ng, nx, nz); }
                             }
-                            if (tu) {
-                                const int tq = pos / p.nK;
-                                const int pr = product_at(p, *tu, tu->r0 + tq);
-                                const int pk = (pos - tq * p.nK) * p.BK;
-                                ptx::tma_prefetch_2d(&tmap_a, pk, pr * p.a_rows_per_r + tx * C_::kTileM + (int)rank * kBM);
-                                const int pb0 = tz * BN + (int)rank * C_::kBNc;
-                                if (!p.b_mn_major) ptx::tma_prefetch_2d(&tmap_b, pk, pr * p.b_rows_per_r + pb0);
-                                else if (p.b_3d) ptx::tma_prefetch_3d(&tmap_b, 0, pr * p.b_rows_per_r + pk, pb0 / p.BK);
+                            if (nr >= 0) {
+                                for (int kk = 0; kk < kPfK && kk < p.nK; ++kk) {
+                                    for (int c = 0; c < CG; ++c) {
+                                        ptx::tma_prefetch_2d(&tmap_a, kk * p.BK,
+                                                             nr * p.a_rows_per_r + nx * C_::kTileM + c * kBM);
+                                        const int bc = nz * BN + c * C_::kBNc;
+                                        if (!p.b_mn_major) ptx::tma_prefetch_2d(&tmap_b, kk * p.BK, nr * p.b_rows_per_r + bc);
+                                        else if (p.b_3d) ptx::tma_prefetch_3d(&tmap_b, 0, nr * p.b_rows_per_r + kk * p.BK, bc / p.BK);
+                                    }
+                                }
                             }
                         }
                         timed_wait(&empty_bar[stage], phase ^ 1, st_empty);
@@ -688,20 +722,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        if (kb == 0 && t == u.r0) it.advance();
                     }
                 }
-                u = un;
-                has_u = has_un;
-                if (has_u) has_un = it.next(un, true);
             }
-            if (p.stats) p.stats[blockIdx.x * 8 + 0] = w_empty;
+            if (p.stats) p.stats[blockIdx.x * kStatsPerCta + 0] = w_empty;
         }
     } else if (warp == 1) {
         // ================================ MMA issuer (leader CTA)
         // The whole warp walks the schedule so that stage / descriptor
         // arithmetic stays in uniform registers; one lane issues the MMAs and
         // the commits (a commit tracks the MMAs of the issuing thread).
-        ptx::setmaxnreg_dec<40>();
+        ptx::setmaxnreg_dec<kRegLo>();
         if (leader) {
             const uint32_t b_lbo = p.BK * 128;            // MN-major: chunk stride
             const uint32_t b_kstep = p.b_mn_major ? (uint32_t)(32 / (p.tf32 ? 4 : 2)) * 128u : 32u;
@@ -721,6 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             unsigned long long w_tempty = 0, w_full = 0;
+            unsigned long long w_kb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             const long long t_start = clock64();
             UnitIter it(p, w, ring, SR_LOCAL, CG);
             Unit u;
@@ -732,7 +765,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (p.tl && lane == 0 && tli < kTlMax) p.tl[((size_t)blockIdx.x * kTlMax + tli) * 4 + 0] = gtimer();
                     const uint32_t d_tmem = tmem_base + acc * BN;
                     for (int kb = 0; kb < p.nK; ++kb) {
-                        timed_wait(&full_bar[stage], phase, (p.stats && lane == 0) ? &w_full : nullptr);
+                        if (p.stats && lane == 0) {
+                            // operand wait by k-block position inside the product
+                            // (0, 1, 2, 3, 4-7, 8-15, 16-31, 32+): stats slots 8..15
+                            const long long t0w = clock64();
+                            ptx::mbar_wait(&full_bar[stage], phase);
+                            const unsigned long long dw = (unsigned long long)(clock64() - t0w);
+                            w_full += dw;
+                            const int bkt = kb < 4 ? kb : kb < 8 ? 4 : kb < 16 ? 5 : kb < 32 ? 6 : 7;
+                            w_kb[bkt] += dw;
+                        } else {
+                            ptx::mbar_wait(&full_bar[stage], phase);
+                        }
                         ptx::tc_fence_after();
                         const uint64_t ad = a_desc0 + (uint64_t)(stage * kStageStep);
                         const uint64_t bd = b_desc0 + (uint64_t)(stage * kStageStep);
@@ -775,13 +819,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (p.stats && lane == 0) {
-                p.stats[blockIdx.x * 8 + 1] = w_tempty;
-                p.stats[blockIdx.x * 8 + 2] = w_full;
-                p.stats[blockIdx.x * 8 + 3] = (unsigned long long)(clock64() - t_start);
+                p.stats[blockIdx.x * kStatsPerCta + 1] = w_tempty;
+                p.stats[blockIdx.x * kStatsPerCta + 2] = w_full;
+                p.stats[blockIdx.x * kStatsPerCta + 3] = (unsigned long long)(clock64() - t_start);
+                for (int b = 0; b < 8; ++b) p.stats[blockIdx.x * kStatsPerCta + 8 + b] = w_kb[b];
             }
         }
     } else if (warp < kEpiWarp0) {
-        ptx::setmaxnreg_dec<40>();   // allocator / idle warps
+        ptx::setmaxnreg_dec<kRegLo>();   // allocator / idle warps
         if constexpr (PF && CG == 2) {
             // ================================ Combine A (PF): warps 2-3 of both CTAs
             // At_r tile = s0 * A_blk0 + s1 * A_blk1 in fp32, one RN rounding to
@@ -849,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ================================ epilogue (both CTAs: own 128 rows)
-        ptx::setmaxnreg_inc<232>();
+        ptx::setmaxnreg_inc<kRegHi>();
         const int ew = warp - kEpiWarp0;           // 0..7
         const int quarter = warp & 3;              // TMEM lane quarter
         const int half = ew >> 2;                  // column half
@@ -1135,7 +1180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int v = w + 1; v <= last_w; ++v) p.flags[v * CG + rank] = 0;
         }
         if (p.stats && ew == 0 && lane == 0) {
-            p.stats[blockIdx.x * 8 + 4] = w_tfull;
+            p.stats[blockIdx.x * kStatsPerCta + 4] = w_tfull;
             (void)t_epi0;
         }
     }
@@ -1149,8 +1194,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.stats && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.stats[blockIdx.x * 8 + 7] = t;
-        p.stats[blockIdx.x * 8 + 5] = (unsigned long long)(clock64() - clk_entry);
+        p.stats[blockIdx.x * kStatsPerCta + 7] = t;
+        p.stats[blockIdx.x * kStatsPerCta + 5] = (unsigned long long)(clock64() - clk_entry);
     }
 }
 

@@ -25,8 +25,8 @@ for env in ENVS:
         os.environ.pop(k, None)
     os.environ.update(env)
     for algo, (M, N, K), ctas, (lo, hi) in CASES:
-        for schedule in (1, 4):
-            if "LCMA_SERPENTINE" in env and schedule == 1:
+        for schedule in (1, 5):
+            if "LCMA_SERPENTINE" in env and schedule == 5:
                 continue          # serpentine rounds exist in the static schedule only
             A, B = inputs.operands(M, N, K, 0, M + 7, N + K, dist="int", lo=lo, hi=hi)
             plan = L.Plan(M, N, K, algo=algo, out_dtype=L.FP32, variant="fused_h", num_ctas=ctas,

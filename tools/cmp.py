@@ -1,6 +1,6 @@
 """Interleaved timing of several (algo, static-B, LCMA_* env) arms on one shape.
 usage: python tools/cmp.py M N K arm [arm ...]
-  arm = name:algo[:s][:variant=NAME][:sched=S][:pf=D][:swz=H][:ENV=v,ENV2=w]
+  arm = name:algo[:s][:variant=NAME][:sched=S][:swz=H][:ENV=v,ENV2=w]
   (s = B precombined offline; ENV knobs need a -DLCMA_DIAG build via LCMA_LIB)
 Prints per-arm median time, effective TFLOP/s and the ratio to the first arm."""
 import os, sys, statistics, json
@@ -33,13 +33,13 @@ for spec in sys.argv[4:]:
     name, algo = parts[0], parts[1]
     static = "s" in parts[2:]
     variant = next((q.split("=", 1)[1] for q in parts[2:] if q.startswith("variant=")), "auto")
-    # plan fields: sched=<schedule>, pf=<prefetch_kblocks>, swz=<raster_rows>
+    # plan fields: sched=<schedule>, swz=<raster_rows>
     kw = {}
     for q in parts[2:]:
-        for key, field in (("sched=", "schedule"), ("pf=", "prefetch_kblocks"), ("swz=", "raster_rows")):
+        for key, field in (("sched=", "schedule"), ("swz=", "raster_rows")):
             if q.startswith(key):
                 kw[field] = int(q.split("=", 1)[1])
-    envp = [q for q in parts[2:] if "=" in q and not q.startswith(("variant=", "sched=", "pf=", "swz="))]
+    envp = [q for q in parts[2:] if "=" in q and not q.startswith(("variant=", "sched=", "swz="))]
     env = dict(kv.split("=") for kv in (envp[-1].split(",") if envp else []))
     keys |= set(env)
     p = L.Plan(M, N, K, dtype=dtype, algo=algo, b_layout=bl, b_static=static, variant=variant, **kw)

@@ -17,9 +17,9 @@ def run(M, N, K, algo, static_b=True, env=None, **kw):
     for _ in range(3):
         (p.gemm_precombined(A, Bt, C, ws) if Bt is not None else p.gemm(A, B, C, ws))
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (1024 * 8))()
-    L.lib().lcma_debug_stats(buf, 1024 * 8)
-    s = np.array(buf[:p.info["ctas"] * 8]).reshape(-1, 8).astype(float)
+    buf = (ctypes.c_ulonglong * (1024 * 16))()
+    L.lib().lcma_debug_stats(buf, 1024 * 16)
+    s = np.array(buf[:p.info["ctas"] * 16]).reshape(-1, 16).astype(float)
     tot = s[:, 3].mean()
     print(f"{algo:10s} {env or ''} total_cyc={tot:.0f} mma_wait_tempty={s[:,1].mean()/tot*100:.1f}% "
           f"mma_wait_full={s[:,2].mean()/tot*100:.1f}% prod_wait_empty={s[:,0].mean()/tot*100:.1f}% "
@@ -38,17 +38,17 @@ def timeline(M, N, K, algo):
     C = p.empty_c(); ws = p.workspace()
     for _ in range(3): p.gemm(A, B, C, ws)
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (1024 * 8))()
-    L.lib().lcma_debug_stats(buf, 1024 * 8)
-    s = np.array(buf[:p.info["ctas"] * 8]).reshape(-1, 8)
+    buf = (ctypes.c_ulonglong * (1024 * 16))()
+    L.lib().lcma_debug_stats(buf, 1024 * 16)
+    s = np.array(buf[:p.info["ctas"] * 16]).reshape(-1, 16)
     t0 = s[:, 6].min()
     st = (s[:, 6] - t0) / 1000.0; en = (s[:, 7] - t0) / 1000.0
     print(f"{algo} cg={p.info['cta_group']} start_us min/med/max {st.min():.1f}/{np.median(st):.1f}/{st.max():.1f}  end_us {en.min():.1f}/{np.median(en):.1f}/{en.max():.1f} mma_cyc_med {np.median(s[:,3]):.0f} sm_GHz {np.median(s[:,5]/(s[:,7]-s[:,6])):.3f}", flush=True)
     print("  sorted starts:", np.round(np.sort(st)[::8], 1).tolist())
 timeline(8192, 14336, 4096, "classical")
-buf = (ctypes.c_ulonglong * (1024 * 8))()
-L.lib().lcma_debug_stats(buf, 1024 * 8)
-s = np.array(buf[:148 * 8]).reshape(-1, 8)
+buf = (ctypes.c_ulonglong * (1024 * 16))()
+L.lib().lcma_debug_stats(buf, 1024 * 16)
+s = np.array(buf[:148 * 16]).reshape(-1, 16)
 np.set_printoptions(linewidth=200)
 print(s[:6])
 t0 = s[:, 6].min()
