@@ -336,7 +336,10 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         }
         p->G = p->nX * p->nZ;
         make_schedule(p, (d.schedule >= 2 && d.schedule <= 5) ? d.schedule : 1);
-        if (variant == LCMA_VARIANT_PRODUCER) p->dyn = 0;   // its combine warps walk the static schedule
+        // the dynamic schedule is instantiated for the 256-column pair kernels
+        // (classical and fused Combine H); the producer-fused variant's
+        // combine warps walk the static schedule
+        if (p->dyn && (p->cg != 2 || p->bn != 256 || variant == LCMA_VARIANT_PRODUCER)) make_schedule(p, 1);
 
         if (variant == LCMA_VARIANT_PRODUCER &&
             (p->cg != 2 || p->bn != 256 || d.M != (int64_t)S.m * p->Mb || d.K != (int64_t)S.k * p->Kb)) {
@@ -667,14 +670,14 @@ lcma_status check_launch(const char* what) {
 
 // The dynamic shared-memory limit is a per-device function attribute: set it
 // once per (instantiation, device).
-template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0>
+template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false>
 lcma_status ensure_smem_attr() {
     static std::once_flag once[kMaxDev];
     static cudaError_t err[kMaxDev];
     const int dv = current_device();
     if (dv < 0) return fail(LCMA_ERR_CUDA, "no current CUDA device (or ordinal >= 64)");
     std::call_once(once[dv], [dv] {
-        err[dv] = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF>,
+        err[dv] = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF, DYN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF>::kSmemBytes);
     });
@@ -799,13 +802,16 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     // an LCMA scheme on 256-column pair tiles); classical / unfused GEMMs use
     // the one without (no 128 live registers reserved in the epilogue)
     const bool regh = !classical && !H && p->cg == 2 && p->bn == 256;
-    if (pf) qf = 0;
+    const bool dyn = p->dyn && sched && !pf;     // the plan only sets dyn for 256-column pair kernels
+    if (pf || dyn) qf = 0;
     lcma_status rs = pf == 2 ? ensure_smem_attr<2, 256, 0, true, 2>()
                    : pf == 1 ? ensure_smem_attr<2, 256, 0, true, 1>()
                    : p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
                                                 : (qf ? ensure_smem_attr<2, 256, 1, true>()
-                                                      : regh ? ensure_smem_attr<2, 256, 0, true>()
-                                                             : ensure_smem_attr<2, 256>()))
+                                                      : regh ? (dyn ? ensure_smem_attr<2, 256, 0, true, 0, true>()
+                                                                    : ensure_smem_attr<2, 256, 0, true>())
+                                                             : (dyn ? ensure_smem_attr<2, 256, 0, false, 0, true>()
+                                                                    : ensure_smem_attr<2, 256>())))
                                 : (p->bn == 128 ? ensure_smem_attr<1, 128>() : ensure_smem_attr<1, 256>());
     if (rs != LCMA_OK) return rs;
     const lcma_dtype dt = p->d.dtype;
@@ -854,14 +860,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
                               b_mn ? 1u : 0u, 0u);
     g.W = p->ctas / p->cg; g.q = p->q; g.tail_c = p->tail_c; g.swz = p->swz;
     g.n_whole = p->n_whole;
-    g.dyn = (p->dyn && sched && !pf) ? 1 : 0;
+    g.dyn = dyn ? 1 : 0;
     g.sched = sched;
-    // product-boundary L2 prefetch: removes the first-k-block stall (MMA
-    // operand wait at k-block 0 of a product 2872 -> 270 cycles, classical
-    // cfg2) but the wait reappears later in the product: no faster (-0..-5 %),
-    // off by default (profiles/r02_schedule.txt)
-    g.pf = 0;
-    if (const char* v = diag_env("LCMA_PF")) g.pf = std::atoi(v);
 
     g.epi_mode = H ? EPI_STORE_H : EPI_FUSED;
     g.out_type = (p->d.out_dtype == LCMA_FP32 || p->d.out_dtype == LCMA_TF32) ? OUT_FP32
@@ -1012,10 +1012,12 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 1, true>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256 && regh) {
         cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
-        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true>, ta, tb, g);
+        e = dyn ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 0, true>, ta, tb, g)
+                : cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256) {
         cfg.dynamicSmemBytes = Cfg<2, 256, 0, true>::kSmemBytes;
-        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256>, ta, tb, g);
+        e = dyn ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, false, 0, true>, ta, tb, g)
+                : cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256>, ta, tb, g);
     } else if (p->cg == 2) {
         cfg.dynamicSmemBytes = Cfg<2, 128>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 128>, ta, tb, g);

@@ -54,8 +54,6 @@ constexpr int kMaxMN = 32;
 constexpr int kTlMax = 512;       // timeline entries per CTA
 constexpr int kStatsPerCta = 16;  // diagnostics: wait counters per CTA (LCMA_STATS)
 constexpr int kSchedDepth = 8;    // dynamic schedule: units published ahead of their consumers
-constexpr int kPfLead = 8;        // product-boundary L2 prefetch: k-blocks ahead ...
-constexpr int kPfK = 4;           // ... of the next product's first kPfK k-blocks
 constexpr int kBarBytes = 512;    // mbarriers, TMEM slot and schedule ring
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -129,7 +127,6 @@ struct GemmParams {
     int dyn;               // 1: whole groups handed out at run time in raster order (ticket
                            //    counter `sched`, broadcast to every role of the pair via a shared ring)
     int* sched;            // dyn: ticket counter (workspace, zero between launches)
-    int pf;                // 1: L2 prefetch of each next product's first k-blocks (pair leader)
     // epilogue
     int epi_mode;
     int out_type;
@@ -198,6 +195,7 @@ enum SchedRole : int { SR_SCHED = 0, SR_LOCAL = 1, SR_PEER = 2 };
 // ticket counter in raster order by the leader's producer and broadcast via
 // the ring (so the groups in flight always form a compact window of the
 // raster, however far the pairs drift apart), then the same static tail.
+template <bool DYN>
 struct UnitIter {
     const GemmParams& p;
     int w;
@@ -209,15 +207,17 @@ struct UnitIter {
     int pend;            // SR_SCHED: ticket drawn, not yet published (-1: none, -2: phase over)
     int pub;             // SR_SCHED: ring slots published so far
     __device__ UnitIter(const GemmParams& p_, int w_, uint32_t ring_ = 0u, int role_ = SR_LOCAL, int cg = 1)
-        : p(p_), w(w_), idx(0), k(0), ring(p_.dyn ? ring_ : 0u), role(role_ | (cg == 2 ? 4 : 0)), pend(-1),
-          pub(0) {
+        : p(p_), w(w_), idx(0), k(0), ring(DYN && p_.dyn ? ring_ : 0u), role(role_ | (cg == 2 ? 4 : 0)),
+          pend(-1), pub(0) {
         int Tt = (p.G - p.n_whole) * p.R;
         if (Tt < 0) Tt = 0;
         t = w * p.tail_c;
         t_end = t + p.tail_c;
         if (t_end > Tt) t_end = Tt;
         if (t > Tt) t = Tt;
-        if (ring) idx = p.q;          // no static rounds
+        if constexpr (DYN) {
+            if (ring) idx = p.q;      // no static rounds
+        }
     }
     // next dynamic group (SR_SCHED: draw + publish; others: read); -1 = over.
     // Warps call this with all lanes; lane 0 (or the single producer lane)
@@ -253,7 +253,7 @@ struct UnitIter {
     // Called by the producer once the current unit's first loads are issued,
     // so the handshake stays off the critical path.
     __device__ void advance() {
-        if (!ring || (role & 3) != SR_SCHED) return;
+        if (!DYN || !ring || (role & 3) != SR_SCHED) return;
         while (pub <= k && pend != -2) {
             const int tk = pend >= 0 ? pend : atomicAdd(p.sched, 1);
             pend = -1;
@@ -289,12 +289,8 @@ struct UnitIter {
         ++k;
         return g;
     }
-    // SR_SCHED: group of its next dynamic unit (published), else -1
-    __device__ int peek() const {
-        return (ring && pub > k) ? (int)ptx::ld_shared_u32(ring + kRingSlot + 4u * (uint32_t)(k % kSchedDepth)) : -1;
-    }
     __device__ bool next(Unit& u, bool single_thread = false) {
-        if (ring) {
+        if (DYN && ring) {
             const int g = dyn_next(single_thread);
             if (g >= 0) {
                 u.g = g;
@@ -437,6 +433,53 @@ __device__ __forceinline__ void store_c_row(const GemmParams& p, long long row, 
     }
 }
 
+// Store 16 consecutive fp32 values of one C row segment (cols c0..c0+15),
+// cropped like store_c_row: the final-contribution paths of the fused
+// epilogue work in 16-column halves so that only 16 temporaries are live
+// next to the register partial (fewer spills).
+__device__ __forceinline__ void store_c_row16(const GemmParams& p, long long row, long long c0,
+                                              const float* v) {
+    if (row >= p.M) return;
+    if (p.debug & 2048) {
+        // diagnostics (results WRONG): the same bytes, fully coalesced -- the
+        // 32 lanes of a warp write 1 KB contiguous of one row band
+        uint32_t w[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) w[h] = pack2(p, v[2 * h], v[2 * h + 1]);
+        uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + (row & ~31ll) * p.ldc + ((c0 * 32) % (p.ldc - 512)) +
+                        (threadIdx.x & 31) * 16;
+        st_v8(dst, w, p.c_cs);
+        return;
+    }
+    if (p.out_type == OUT_FP32) {
+        float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + c0;
+        if (p.c_v8 && c0 + 16 <= p.N) {
+            st_v8(dst, reinterpret_cast<const uint32_t*>(v), p.c_cs);
+            st_v8(dst + 8, reinterpret_cast<const uint32_t*>(v + 8), p.c_cs);
+            return;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+            if (c0 + e < p.N)
+                *reinterpret_cast<float4*>(dst + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        }
+    } else {
+        uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + row * p.ldc + c0;
+        uint32_t w[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) w[h] = pack2(p, v[2 * h], v[2 * h + 1]);
+        if (p.c_v8 && c0 + 16 <= p.N) {
+            st_v8(dst, w, p.c_cs);
+            return;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; e += 8) {
+            if (c0 + e < p.N)
+                *reinterpret_cast<uint4*>(dst + e) = make_uint4(w[e / 2], w[e / 2 + 1], w[e / 2 + 2], w[e / 2 + 3]);
+        }
+    }
+}
+
 __device__ __forceinline__ uint32_t pack2(const GemmParams& p, float a, float b) {
     if (p.out_type == OUT_BF16) {
         __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
@@ -509,7 +552,7 @@ __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, unsig
 }
 
 // ------------------------------------------------------------ the kernel
-template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0>
+template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
@@ -601,9 +644,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t opol = oh == 2 || oh == 3 ? ptx::policy_evict_last() : ptx::policy_evict_first();
             const uint64_t opol_b = oh == 2 || oh == 4 ? ptx::policy_evict_last() : ptx::policy_evict_first();
             const bool ohint = oh != 0;
-            UnitIter it(p, w, ring, leader ? SR_SCHED : SR_PEER, CG);
+            UnitIter<DYN> it(p, w, ring, leader ? SR_SCHED : SR_PEER, CG);
             Unit u;
-            const int pf_at = p.nK > kPfLead ? p.nK - kPfLead : 0;
             while (it.next(u, true)) {
                 int x, z;
                 group_xz(p, u.g, x, z);
@@ -612,29 +654,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int a_row = r * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
                     const int b_col0 = z * BN + (int)rank * C_::kBNc;
                     for (int kb = 0; kb < p.nK; ++kb) {
-                        if (p.pf && leader && kb == pf_at) {
-                            // L2 prefetch of the first k-blocks of the next product (its
-                            // panels are new: their first loads would miss L2), for both
-                            // CTAs of the pair, kPfLead k-blocks before they are needed
-                            int nr = -1, nx = x, nz = z;
-                            if (t + 1 < u.r1) {
-                                nr = product_at(p, u, t + 1);
-                            } else {
-                                const int ng = it.peek();
-                                if (ng >= 0) { nr = p.rperm[0]; group_xz(p, ng, nx, nz); }
-                            }
-                            if (nr >= 0) {
-                                for (int kk = 0; kk < kPfK && kk < p.nK; ++kk) {
-                                    for (int c = 0; c < CG; ++c) {
-                                        ptx::tma_prefetch_2d(&tmap_a, kk * p.BK,
-                                                             nr * p.a_rows_per_r + nx * C_::kTileM + c * kBM);
-                                        const int bc = nz * BN + c * C_::kBNc;
-                                        if (!p.b_mn_major) ptx::tma_prefetch_2d(&tmap_b, kk * p.BK, nr * p.b_rows_per_r + bc);
-                                        else if (p.b_3d) ptx::tma_prefetch_3d(&tmap_b, 0, nr * p.b_rows_per_r + kk * p.BK, bc / p.BK);
-                                    }
-                                }
-                            }
-                        }
                         timed_wait(&empty_bar[stage], phase ^ 1, st_empty);
                         uint8_t* sa = smem + stage * C_::kStageBytes;
                         uint8_t* sb = sa + C_::kABytes;
@@ -722,7 +741,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
-                        if (kb == 0 && t == u.r0) it.advance();
+                        if constexpr (DYN) {
+                            if (kb == 0 && t == u.r0) it.advance();
+                        }
                     }
                 }
             }
@@ -755,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             unsigned long long w_tempty = 0, w_full = 0;
             unsigned long long w_kb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             const long long t_start = clock64();
-            UnitIter it(p, w, ring, SR_LOCAL, CG);
+            UnitIter<DYN> it(p, w, ring, SR_LOCAL, CG);
             Unit u;
             int tli = 0;
             while (it.next(u)) {
@@ -837,7 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool bf16 = ((p.idesc >> 7) & 7u) == 1u;   // kind::f16 a_format: 1 = bf16, 0 = fp16
             int stage = 0;
             uint32_t phase = 0;
-            UnitIter it(p, w);
+            UnitIter<false> it(p, w);
             Unit u;
             while (it.next(u)) {
                 for (int t = u.r0; t < u.r1; ++t) {
@@ -913,7 +934,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kPregCols = REGH ? BN / 2 : 1;
         float preg[kPregCols];
         int tl_i = 0;             // timeline product index (diagnostics)
-        UnitIter it(p, w, ring, leader ? SR_LOCAL : SR_PEER, CG);
+        UnitIter<DYN> it(p, w, ring, leader ? SR_LOCAL : SR_PEER, CG);
         Unit u;
         while (it.next(u)) {
             int x, z;
@@ -1002,7 +1023,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                                     for (int e = 0; e < 32; ++e)
                                         pr[e] = (first ? 0.f : pr[e]) + sw * __uint_as_float(raw[e]);
-                                    if (in_range && !(p.debug & 128)) store_c_row(p, (long long)i * p.Mb + brow, ccol, pr);
+                                    if (in_range && !(p.debug & 128)) {
+                                        store_c_row16(p, (long long)i * p.Mb + brow, ccol, pr);
+                                        store_c_row16(p, (long long)i * p.Mb + brow, ccol + 16, pr + 16);
+                                    }
                                 } else if (first) {
 #pragma unroll
                                     for (int e = 0; e < 32; ++e) pr[e] = sw * __uint_as_float(raw[e]);
@@ -1016,17 +1040,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 // shared partial: plain loads / stores in program order
                                 float* sp = psmem;
                                 if (final_here) {
-                                    float v[32];
 #pragma unroll
-                                    for (int e = 0; e < 32; e += 4) {
-                                        float4 o = first ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                                         : *reinterpret_cast<const float4*>(sp + partial_off(row, c4 + (e >> 2)));
-                                        v[e] = o.x + sw * __uint_as_float(raw[e]);
-                                        v[e + 1] = o.y + sw * __uint_as_float(raw[e + 1]);
-                                        v[e + 2] = o.z + sw * __uint_as_float(raw[e + 2]);
-                                        v[e + 3] = o.w + sw * __uint_as_float(raw[e + 3]);
+                                    for (int hh = 0; hh < 32; hh += 16) {
+                                        float v[16];
+#pragma unroll
+                                        for (int e = 0; e < 16; e += 4) {
+                                            float4 o = first ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                             : *reinterpret_cast<const float4*>(sp + partial_off(row, c4 + ((hh + e) >> 2)));
+                                            v[e] = o.x + sw * __uint_as_float(raw[hh + e]);
+                                            v[e + 1] = o.y + sw * __uint_as_float(raw[hh + e + 1]);
+                                            v[e + 2] = o.z + sw * __uint_as_float(raw[hh + e + 2]);
+                                            v[e + 3] = o.w + sw * __uint_as_float(raw[hh + e + 3]);
+                                        }
+                                        if (in_range && !(p.debug & 128))
+                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v);
                                     }
-                                    if (in_range && !(p.debug & 128)) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
                                 } else {
 #pragma unroll
                                     for (int e = 0; e < 32; e += 4) {
@@ -1044,27 +1072,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 float* pt = whole ? partial_tile<BN>(p, slot, home, true)
                                                   : partial_tile<BN>(p, slot, ij, false);
                                 if (final_here) {
-                                    // last contribution: C_ij = partial + w*H_r, rounded once;
-                                    // the 8 partial loads are issued together
-                                    float v[32];
+                                    // last contribution: C_ij = partial + w*H_r, rounded once,
+                                    // in two 16-column halves (4 partial loads issued together;
+                                    // only 16 temporaries live next to the register partial)
 #pragma unroll
-                                    for (int e = 0; e < 32; ++e) v[e] = sw * __uint_as_float(raw[e]);
-                                    if (!first) {
-                                        // two batches of 4 loads (register budget: the
-                                        // register partial, H and v are live here)
+                                    for (int hh = 0; hh < 32; hh += 16) {
+                                        float v[16];
 #pragma unroll
-                                        for (int b = 0; b < 8; b += 4) {
+                                        for (int e = 0; e < 16; ++e) v[e] = sw * __uint_as_float(raw[hh + e]);
+                                        if (!first) {
                                             float4 o[4];
 #pragma unroll
-                                            for (int q = 0; q < 4; ++q) o[q] = ld_cg_f4(pt + partial_off(row, c4 + b + q));
+                                            for (int q = 0; q < 4; ++q) o[q] = ld_cg_f4(pt + partial_off(row, c4 + (hh >> 2) + q));
 #pragma unroll
                                             for (int q = 0; q < 4; ++q) {
-                                                v[4 * (b + q)] += o[q].x; v[4 * (b + q) + 1] += o[q].y;
-                                                v[4 * (b + q) + 2] += o[q].z; v[4 * (b + q) + 3] += o[q].w;
+                                                v[4 * q] += o[q].x; v[4 * q + 1] += o[q].y;
+                                                v[4 * q + 2] += o[q].z; v[4 * q + 3] += o[q].w;
                                             }
                                         }
+                                        if (in_range && !(p.debug & 128))
+                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v);
                                     }
-                                    if (in_range && !(p.debug & 128)) store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
                                     if (!first && p.discard) {
                                         __syncwarp();      // the 8 lanes sharing a line have read it
                                         if ((row & 7) == 0) discard_lines(pt, row, c4, 8);
@@ -1136,42 +1164,80 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+            // merge: C_ij = own partial + the contributing segments' partials in
+            // unit order (fixed: bitwise deterministic).  The source tiles of a
+            // 16-column slice are loaded in batches of 4 before any add, so one
+            // L2 round trip serves up to four partials (the tail used to
+            // serialise ~100 dependent round trips per thread)
             for (int ij = 0; ij < mn; ++ij) {
                 const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
+                // sources in merge order: own (if this segment touched C_ij), then
+                // units w+1 .. last_w whose positions contribute to C_ij (bit d of
+                // cm[] = unit w+1+d; last_w - w < R <= kMaxR = 128)
+                uint64_t cm[2] = {0ull, 0ull};
+                for (int vw = w + 1; vw <= last_w; ++vw) {
+                    int lo = (int)((long long)vw * p.tail_c - Tt_base);
+                    int hi = lo + p.tail_c;
+                    if (lo < 0) lo = 0;
+                    if (hi > p.R) hi = p.R;
+                    bool contributes = false;
+                    for (int t = lo; t < hi; ++t)
+                        if (p.Wc[p.rperm[t] * mn + ij]) { contributes = true; break; }
+                    const int d = vw - w - 1;
+                    if (contributes) cm[d >> 6] |= 1ull << (d & 63);
+                }
+                const bool own = (seen >> ij) & 1u;
 #pragma unroll 1
-                for (int ch = 0; ch < (BN / 2) / 32; ++ch) {
-                    const int col0 = half * (BN / 2) + ch * 32;
-                    float v[32];
+                for (int ch = 0; ch < (BN / 2) / 16; ++ch) {
+                    const int col0 = half * (BN / 2) + ch * 16;
+                    float v[16];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
-                    if ((seen >> ij) & 1u) {
-                        const float* pt = partial_tile<BN>(p, blockIdx.x, ij, false);
+                    for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                    uint64_t m0 = cm[0], m1 = cm[1];
+                    bool take_own = own;
+                    for (;;) {
+                        // next batch of up to 4 source slots, in merge order
+                        int src[4];
+                        int ns = 0;
 #pragma unroll
-                        for (int e = 0; e < 32; e += 4) {
-                            float4 o = ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
-                            v[e] += o.x; v[e + 1] += o.y; v[e + 2] += o.z; v[e + 3] += o.w;
+                        for (int q = 0; q < 4; ++q) {
+                            int sl = -1;
+                            if (take_own) {
+                                sl = (int)blockIdx.x;
+                                take_own = false;
+                            } else if (m0 | m1) {
+                                const int d = m0 ? __ffsll((long long)m0) - 1 : 64 + __ffsll((long long)m1) - 1;
+                                if (d < 64) m0 &= m0 - 1; else m1 &= m1 - 1;
+                                sl = (int)gridDim.x + (w + 1 + d) * CG + (int)rank;
+                            }
+                            src[q] = sl;
+                            ns += sl >= 0;
                         }
-                    }
-                    for (int vw = w + 1; vw <= last_w; ++vw) {
-                        // does unit vw's segment (positions [lo, hi)) contribute to C_ij?
-                        long long lo = (long long)vw * p.tail_c - Tt_base;
-                        long long hi = lo + p.tail_c;
-                        if (lo < 0) lo = 0;
-                        if (hi > p.R) hi = p.R;
-                        bool contributes = false;
-                        for (long long t = lo; t < hi; ++t)
-                            if (p.Wc[p.rperm[t] * mn + ij]) { contributes = true; break; }
-                        if (!contributes) continue;
-                        const float* pt = partial_tile<BN>(p, (int)gridDim.x + vw * CG + (int)rank, ij, false);
+                        if (ns == 0) break;
+                        float4 o[4][4];
 #pragma unroll
-                        for (int e = 0; e < 32; e += 4) {
-                            float4 o = ld_cg_f4(pt + partial_off(row, (col0 + e) >> 2));
-                            v[e] += o.x; v[e + 1] += o.y; v[e + 2] += o.z; v[e + 3] += o.w;
+                        for (int q = 0; q < 4; ++q) {
+                            // (a valid address for every q: empty entries re-read the
+                            // first source and are discarded)
+                            const float* pt = partial_tile<BN>(p, src[q] >= 0 ? src[q] : src[0], ij, false);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) o[q][e] = ld_cg_f4(pt + partial_off(row, (col0 >> 2) + e));
                         }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            if (src[q] >= 0) {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    v[4 * e] += o[q][e].x; v[4 * e + 1] += o[q][e].y;
+                                    v[4 * e + 2] += o[q][e].z; v[4 * e + 3] += o[q][e].w;
+                                }
+                            }
+                        }
+                        if (ns < 4) break;
                     }
                     const long long ccol = (long long)j * p.Nb + (long long)z * BN + col0;
                     if (brow < p.Mb && ccol < (long long)(j + 1) * p.Nb)
-                        store_c_row(p, (long long)i * p.Mb + brow, ccol, v);
+                        store_c_row16(p, (long long)i * p.Mb + brow, ccol, v);
                 }
             }
             // all reads done -> reset the flags for the next launch

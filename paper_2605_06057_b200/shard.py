@@ -2,9 +2,17 @@
 "partitioned across the 8xB200 box by block-rows of A and C, which needs no
 communication beyond an optional NCCL all-gather of C").
 
-Rank p owns rows [p*M/P, (p+1)*M/P) of A and C; B is replicated; each rank
-plans its own LCMA on (M/P, N, K).  The only collective is the optional
-all-gather of the contiguous C row blocks, which *is* row-major C.
+Plain partition: rank p owns rows [p*M/P, (p+1)*M/P) of A and C; B is
+replicated; each rank plans its own LCMA on (M/P, N, K).  The only collective
+is the optional all-gather of the contiguous C row blocks, which *is*
+row-major C.
+
+Banded partition (the overlapped all-gather of SURVEY 8(f) 3): the rows are
+cut into `bands` bands of P*h rows and rank p owns rows
+[(c*P + p)*h, (c*P + p + 1)*h) of every band c.  Each rank computes its
+bands one after the other; band c of all ranks is then one contiguous block
+of C, so a single all_gather_into_tensor lands it in place (no staging copy,
+no strided views) while band c+1 is being computed.
 """
 from __future__ import annotations
 
@@ -31,49 +39,54 @@ def allgather_rows(C_local, M: int, group=None):
     return out
 
 
-def band_rows(rows: int, n_bands: int, align: int = 256):
-    """Split [0, rows) into <= n_bands contiguous bands of `align`-multiple
-    height (the last band takes the remainder)."""
-    if rows < 1 or n_bands < 1:
-        raise ValueError("rows and n_bands must be >= 1")
-    per = -(-rows // n_bands)                  # ceil(rows / n_bands)
-    step = -(-per // align) * align            # rounded up to the alignment
-    out, r = [], 0
-    while r < rows:
-        out.append((r, min(rows, r + step)))
-        r += step
-    return out
+def band_height(M: int, world: int, bands: int) -> int:
+    """Rows per (rank, band) of the banded partition; M must split evenly."""
+    if world < 1 or bands < 1 or M < 1:
+        raise ValueError("M, world and bands must be >= 1")
+    if M % (world * bands):
+        raise ValueError("banded partition needs M divisible by world * bands")
+    return M // (world * bands)
 
 
-def gemm_allgather_overlapped(compute_band, C_local, C_full, bands, group=None, comm_stream=None):
-    """All-gather of C overlapped with the compute of later row bands
-    (SURVEY 8(f) item 3).
+def banded_rows(M: int, world: int, rank: int, bands: int):
+    """Global row ranges [r0, r1) that rank `rank` owns, band by band."""
+    if not 0 <= rank < world:
+        raise ValueError("bad rank / world size")
+    h = band_height(M, world, bands)
+    return [((c * world + rank) * h, (c * world + rank + 1) * h) for c in range(bands)]
 
-    compute_band(r0, r1) enqueues rows [r0, r1) of this rank's block C_local on
-    the current stream.  After each band the same band of every rank is
-    gathered into C_full (rank q's rows start at q * C_local.shape[0]) on
-    `comm_stream` (a side CUDA stream; None on CPU), so band c's transfer
-    overlaps band c+1's compute.  Returns after the current stream has been
-    ordered after every gather."""
+
+def gemm_allgather_banded(compute_band, C_local, C_full, bands: int, group=None, comm_stream=None):
+    """All-gather of C overlapped with the compute of later bands.
+
+    C_local holds this rank's bands stacked ([bands * h, N], band c at rows
+    c*h .. c*h+h); compute_band(c) enqueues band c into it on the current
+    stream.  After band c, all_gather_into_tensor(C_full[c*P*h:(c+1)*P*h],
+    C_local[c*h:(c+1)*h]) runs on `comm_stream` (a side CUDA stream; None on
+    CPU), so band c's transfer overlaps band c+1's compute.  Returns after the
+    current stream has been ordered after every gather."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    ml = C_local.shape[0]
-    if C_full.shape[0] != ml * world:
-        raise ValueError("C_full must hold world * rows_per_rank rows")
+    if C_local.shape[0] % bands:
+        raise ValueError("C_local rows must be bands * h")
+    h = C_local.shape[0] // bands
+    if C_full.shape[0] != h * bands * world:
+        raise ValueError("C_full must hold world * bands * h rows")
     cuda = C_local.is_cuda
     works = []
-    for r0, r1 in bands:
-        compute_band(r0, r1)
-        outs = [C_full[q * ml + r0:q * ml + r1] for q in range(world)]
+    for c in range(bands):
+        compute_band(c)
+        dst = C_full[c * world * h:(c + 1) * world * h]
+        src = C_local[c * h:(c + 1) * h]
         if cuda:
             ev = torch.cuda.Event()
             ev.record()
             with torch.cuda.stream(comm_stream):
                 comm_stream.wait_event(ev)
-                works.append(dist.all_gather(outs, C_local[r0:r1], group=group, async_op=True))
+                works.append(dist.all_gather_into_tensor(dst, src, group=group, async_op=True))
         else:
-            dist.all_gather(outs, C_local[r0:r1], group=group)
+            dist.all_gather_into_tensor(dst, src, group=group)
     for w in works:
         w.wait()
     if cuda:

@@ -67,48 +67,57 @@ def test_gloo_world2_block_rows_allgather():
     assert np.array_equal(C, O.gemm_i64(A.to(torch.int64).numpy(), B.to(torch.int64).numpy()))
 
 
-def _worker_overlap(rank, world, port, M, N, K, out):
+def _worker_banded(rank, world, port, M, N, K, bands, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import oracle as O
     from paper_2605_06057_b200 import inputs
     A, B = inputs.operands(M, N, K, 2, 71, 72, dist="int", lo=-2, hi=2)
-    r0, r1 = shard.row_block(M, world, rank)
-    Ai, Bi = A[r0:r1].to(torch.int64).numpy(), B.to(torch.int64).numpy()
-    C_local = torch.zeros(r1 - r0, N, dtype=torch.int64)
+    Bi = B.to(torch.int64).numpy()
+    rows = shard.banded_rows(M, world, rank, bands)
+    h = shard.band_height(M, world, bands)
+    C_local = torch.zeros(bands * h, N, dtype=torch.int64)
     C_full = torch.full((M, N), -999, dtype=torch.int64)
     order = []
 
-    def compute_band(b0, b1):
-        order.append((b0, b1))
-        C_local[b0:b1] = torch.from_numpy(O.gemm_i64(Ai[b0:b1], Bi))
+    def compute_band(c):
+        # this rank's band c = global rows rows[c] (the oracle stands in for
+        # the GPU kernel: the test covers partition, order and placement)
+        order.append(c)
+        r0, r1 = rows[c]
+        C_local[c * h:(c + 1) * h] = torch.from_numpy(O.gemm_i64(A[r0:r1].to(torch.int64).numpy(), Bi))
 
-    bands = shard.band_rows(r1 - r0, 3, align=8)
-    shard.gemm_allgather_overlapped(compute_band, C_local, C_full, bands)
-    assert order == bands
+    shard.gemm_allgather_banded(compute_band, C_local, C_full, bands)
+    assert order == list(range(bands))
     if rank == 0:
         out.put(C_full.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_band_rows():
-    assert shard.band_rows(4096, 4) == [(0, 1024), (1024, 2048), (2048, 3072), (3072, 4096)]
-    assert shard.band_rows(1000, 3, align=256) == [(0, 512), (512, 1000)]
-    assert shard.band_rows(100, 8, align=256) == [(0, 100)]
+def test_banded_partition():
+    # every row owned exactly once; band c of all ranks is one contiguous block
+    for (M, P, bands) in [(96, 2, 3), (32768, 8, 2), (32768, 2, 4), (64, 1, 4)]:
+        h = shard.band_height(M, P, bands)
+        owned = sorted(r for p in range(P) for r0, r1 in shard.banded_rows(M, P, p, bands) for r in range(r0, r1))
+        assert owned == list(range(M))
+        for c in range(bands):
+            starts = sorted(shard.banded_rows(M, P, p, bands)[c][0] for p in range(P))
+            assert starts == [c * P * h + p * h for p in range(P)]
     with pytest.raises(ValueError):
-        shard.band_rows(0, 2)
+        shard.band_height(100, 3, 2)
 
 
-def test_gloo_world2_overlapped_band_allgather():
-    # cfg5's all-gather of C in row bands: every band of every
-    # rank lands at its row offset; the result equals the single-process GEMM
+@pytest.mark.parametrize("bands", [1, 3])
+def test_gloo_world2_banded_overlapped_allgather(bands):
+    # cfg5's all-gather of C overlapped band by band with
+    # all_gather_into_tensor straight into C: equals the single-process GEMM
     M, N, K = 96, 40, 24
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_overlap, args=(r, 2, port, M, N, K, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker_banded, args=(r, 2, port, M, N, K, bands, q)) for r in range(2)]
     for p in procs:
         p.start()
     C = q.get(timeout=120)
