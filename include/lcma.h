@@ -122,7 +122,9 @@ typedef struct {
                                  5 whole groups handed out in raster order at run
                                    time (ticket counter in the workspace: the groups
                                    in flight stay a compact window of the raster)
-                                   + the split tail                                */
+                                   + the split tail's segments handed out at run
+                                   time to the pairs that finish first;
+                                 6 static lockstep rounds + the run-time tail      */
     int32_t num_ctas;         /* 0 = one per SM                                    */
     const lcma_hw_profile* hw;/* NULL -> built-in B200 profile                     */
     int32_t decision_model;   /* algo AUTO: 0 = this build's B200-calibrated model

@@ -102,7 +102,7 @@ struct lcma_plan_s {
     int BK, e;
     int nX, nZ, G, nK;
     int ctas, cg, bn, q, tail_c, swz;
-    int n_whole, dyn;
+    int n_whole, dyn, dyn_tail;
     size_t off_sched, off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
     size_t off_inner = 0;          // two-level: the inner plan's partial slots + flags
     lcma_plan_s* inner = nullptr;  // two-level: fused GEMM plan of the base scheme
@@ -142,6 +142,7 @@ void make_schedule(lcma_plan_s* p, int mode) {
     const int R = p->sch.R;
     const int W = p->ctas / p->cg;
     p->dyn = 0;
+    p->dyn_tail = 0;
     if (mode == 2) {
         p->q = 0;                              // paper: contiguous split-group chunks
     } else if (mode == 3) {
@@ -156,6 +157,9 @@ void make_schedule(lcma_plan_s* p, int mode) {
         // cfg2, -8..-16 % (classical) / -2..+9 % (Strassen) at cfg5,
         // profiles/r02_schedule.txt), so the default (1 = 4) stays static
         p->dyn = mode == 5 ? 1 : 0;
+        // modes 5 and 6: the split tail's segments are handed out at run time
+        // to the pairs that finish their whole groups first
+        p->dyn_tail = (mode == 5 || mode == 6) ? 1 : 0;
     }
     p->n_whole = (int)std::min<long long>((long long)p->q * W, p->G);
     // R == 1 (classical): nothing to split, every group is handed out whole
@@ -335,11 +339,12 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             return fail(LCMA_ERR_NOT_SUPPORTED, "problem too large for 32-bit tile coordinates");
         }
         p->G = p->nX * p->nZ;
-        make_schedule(p, (d.schedule >= 2 && d.schedule <= 5) ? d.schedule : 1);
+        make_schedule(p, (d.schedule >= 2 && d.schedule <= 6) ? d.schedule : 1);
         // the dynamic schedule is instantiated for the 256-column pair kernels
         // (classical and fused Combine H); the producer-fused variant's
         // combine warps walk the static schedule
-        if (p->dyn && (p->cg != 2 || p->bn != 256 || variant == LCMA_VARIANT_PRODUCER)) make_schedule(p, 1);
+        if ((p->dyn || p->dyn_tail) && (p->cg != 2 || p->bn != 256 || variant == LCMA_VARIANT_PRODUCER))
+            make_schedule(p, 1);
 
         if (variant == LCMA_VARIANT_PRODUCER &&
             (p->cg != 2 || p->bn != 256 || d.M != (int64_t)S.m * p->Mb || d.K != (int64_t)S.k * p->Kb)) {
@@ -802,7 +807,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     // an LCMA scheme on 256-column pair tiles); classical / unfused GEMMs use
     // the one without (no 128 live registers reserved in the epilogue)
     const bool regh = !classical && !H && p->cg == 2 && p->bn == 256;
-    const bool dyn = p->dyn && sched && !pf;     // the plan only sets dyn for 256-column pair kernels
+    // the plan only sets dyn / dyn_tail for 256-column pair kernels
+    const bool dyn = (p->dyn || p->dyn_tail) && sched && !pf;
     if (pf || dyn) qf = 0;
     lcma_status rs = pf == 2 ? ensure_smem_attr<2, 256, 0, true, 2>()
                    : pf == 1 ? ensure_smem_attr<2, 256, 0, true, 1>()
@@ -860,7 +866,9 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
                               b_mn ? 1u : 0u, 0u);
     g.W = p->ctas / p->cg; g.q = p->q; g.tail_c = p->tail_c; g.swz = p->swz;
     g.n_whole = p->n_whole;
-    g.dyn = dyn ? 1 : 0;
+    g.dyn = dyn && p->dyn ? 1 : 0;
+    g.dyn_tail = dyn && p->dyn_tail ? 1 : 0;
+    g.n_own = p->info.split_groups;
     g.sched = sched;
 
     g.epi_mode = H ? EPI_STORE_H : EPI_FUSED;

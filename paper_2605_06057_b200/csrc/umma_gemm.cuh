@@ -126,7 +126,9 @@ struct GemmParams {
     int n_whole;           // groups processed whole before the split tail (static: q * W, <= G)
     int dyn;               // 1: whole groups handed out at run time in raster order (ticket
                            //    counter `sched`, broadcast to every role of the pair via a shared ring)
-    int* sched;            // dyn: ticket counter (workspace, zero between launches)
+    int* sched;            // dyn / dyn_tail: ticket counters [2] (workspace, zero between launches)
+    int dyn_tail;          // 1: tail segments handed out at run time (DYN instantiation)
+    int n_own;             // split groups of the tail (= owner segments)
     // epilogue
     int epi_mode;
     int out_type;
@@ -174,112 +176,156 @@ struct GemmParams {
 struct Unit {
     int g, r0, r1, role;
     int rev;             // whole group of an odd lockstep round: products in reverse order
+    int seg;             // split tail: segment index (its partial slot / flag); static: the unit slot w
 };
 
 // Shared-memory ring through which the pair leader's producer (the
-// scheduler) hands dynamically drawn whole groups to every other role of the
+// scheduler) hands run-time scheduling decisions to every other role of the
 // pair.  One 32-bit shared address `ring` locates it (kept small: the
 // producer / MMA warps run with few registers): full[d] mbarriers at
 // ring + 8d (armed by the scheduler, locally and in the peer CTA), empty[d]
 // at ring + 8D + 8d (leader only: the consumers that have read slot d), and
-// slot[d] (int, group of the k-th dynamic unit with k % D == d; -1: the
-// dynamic phase is over) at ring + 16D + 4d.
+// slot[d] (int value of the k-th decision with k % D == d) at ring + 16D + 4d.
+// Values: g >= 0 a whole group, -2 - s tail segment s, -1 the end.
 constexpr uint32_t kRingFull = 0, kRingEmpty = 8 * kSchedDepth, kRingSlot = 16 * kSchedDepth;
 constexpr int kRingBytes = 20 * kSchedDepth;
 enum SchedRole : int { SR_SCHED = 0, SR_LOCAL = 1, SR_PEER = 2 };
 
 // Enumerates the units of work-unit slot `w` in processing order.  Every role
 // of the CTA (producer, MMA, epilogue) and both CTAs of a pair walk the same
-// sequence.  Static mode (dyn = 0): lockstep rounds, group idx*W + w, then the
-// split tail.  Dynamic mode: the first n_whole groups are drawn from a global
-// ticket counter in raster order by the leader's producer and broadcast via
-// the ring (so the groups in flight always form a compact window of the
-// raster, however far the pairs drift apart), then the same static tail.
+// sequence.
+//  DYN = false: lockstep rounds, group idx*W + w (P:391-396 cache-aware
+//    reading 11), then unit w's segment of the split tail.
+//  DYN = true: the pair leader's producer decides and broadcasts through the
+//    ring: whole groups either in the same static rounds (dyn = 0) or drawn
+//    from a ticket counter in raster order (dyn = 1, the groups in flight
+//    stay a compact window of the raster), then tail segments drawn from a
+//    second counter (dyn_tail), so the pairs that finish their whole groups
+//    first take the tail: the owner of a split group waits only for pairs
+//    that were free, not for the slowest ones.
 template <bool DYN>
 struct UnitIter {
     const GemmParams& p;
-    int w;
-    int idx;             // lockstep round index (static), then tail
-    int t, t_end;        // tail tile cursor (G * R < 2^31)
-    int k;               // dynamic units consumed / published so far
-    uint32_t ring;       // shared address of the ring; 0: static schedule only
-    int role;            // SchedRole | (CG == 2 ? 4 : 0)
-    int pend;            // SR_SCHED: ticket drawn, not yet published (-1: none, -2: phase over)
-    int pub;             // SR_SCHED: ring slots published so far
+    int idx;             // lockstep round index
+    int t;               // tail tile cursor (G * R < 2^31)
+    int seg;             // tail segment being enumerated ([t, end of seg))
+    int k;               // ring decisions consumed so far
+    uint32_t ring;       // shared address of the ring (DYN)
+    int pend;            // SR_SCHED: whole-group ticket drawn ahead (-1: none)
+    int st;              // bits 0-1 SchedRole, 2 pair, 3-4 phase (SR_SCHED: 0 whole groups,
+                         // 1 tail segments, 2 decided the end, 3 published it), 5 published
+                         // one decision ahead of k
     __device__ UnitIter(const GemmParams& p_, int w_, uint32_t ring_ = 0u, int role_ = SR_LOCAL, int cg = 1)
-        : p(p_), w(w_), idx(0), k(0), ring(DYN && p_.dyn ? ring_ : 0u), role(role_ | (cg == 2 ? 4 : 0)),
-          pend(-1), pub(0) {
-        int Tt = (p.G - p.n_whole) * p.R;
-        if (Tt < 0) Tt = 0;
-        t = w * p.tail_c;
-        t_end = t + p.tail_c;
-        if (t_end > Tt) t_end = Tt;
-        if (t > Tt) t = Tt;
-        if constexpr (DYN) {
-            if (ring) idx = p.q;      // no static rounds
-        }
+        : p(p_), idx(0), t(0), seg(DYN ? -1 : w_), k(0), ring(ring_), pend(-1), st(role_ | (cg == 2 ? 4 : 0)) {
+        if constexpr (!DYN) t = seg_begin(w_);
     }
-    // next dynamic group (SR_SCHED: draw + publish; others: read); -1 = over.
-    // Warps call this with all lanes; lane 0 (or the single producer lane)
-    // does the arrivals.
-    // SR_SCHED: publish ring slot `pub` with ticket tk (group, or -1 once the
-    // whole-group phase is over); returns the group.
-    __device__ int publish(int tk) {
+    __device__ int unit_w() const { return (int)blockIdx.x / ((st & 4) ? 2 : 1); }
+    __device__ int tail_tiles() const {
+        const int Tt = (p.G - p.n_whole) * p.R;
+        return Tt < 0 ? 0 : Tt;
+    }
+    __device__ int seg_begin(int s) const {
+        const int b = s * p.tail_c, Tt = tail_tiles();
+        return b < Tt ? b : Tt;
+    }
+    __device__ int seg_end() const {
+        const int e = (seg + 1) * p.tail_c, Tt = tail_tiles();
+        return e < Tt ? e : Tt;
+    }
+    __device__ int phase() const { return (st >> 3) & 3; }
+    __device__ void set_phase(int ph) { st = (st & ~(3 << 3)) | (ph << 3); }
+    // ---- SR_SCHED: the next decision, in order (whole groups, tail, end)
+    __device__ int decide() {
+        const int W = (int)gridDim.x / ((st & 4) ? 2 : 1);
+        if (phase() == 0) {
+            if (p.dyn) {
+                const int tk = pend >= 0 ? pend : atomicAdd(p.sched, 1);
+                pend = -1;
+                // every unit draws exactly one failing ticket; the last one
+                // drawn (n_whole + W - 1) resets the counter for the next launch
+                if (tk == p.n_whole + W - 1) atomicExch(p.sched, 0);
+                if (tk < p.n_whole) return tk;
+            } else if (idx < p.q && idx * p.W + unit_w() < p.G) {
+                return (idx++) * p.W + unit_w();
+            }
+            set_phase(1);
+        }
+        if (phase() == 1) {
+            const int Tt = tail_tiles();
+            const int nseg = Tt > 0 ? (Tt + p.tail_c - 1) / p.tail_c : 0;
+            if (p.dyn_tail) {
+                // A pair that draws an owner segment (the start of a split group)
+                // draws nothing after it: its epilogue will wait there for the
+                // group's other segments, which must then belong to other pairs
+                // (a later segment of its own would deadlock).  Every other pair
+                // ends with one failing ticket; the last of those (nseg +
+                // W - n_own - 1) resets the counter for the next launch.
+                const int tk = atomicAdd(p.sched + 1, 1);
+                if (tk < nseg) {
+                    const int b = tk * p.tail_c;
+                    const int e = b + p.tail_c < Tt ? b + p.tail_c : Tt;
+                    const int last_start = ((e - 1) / p.R) * p.R;       // last group starting before e
+                    if (last_start >= b && last_start + p.R > e) set_phase(2);
+                    return -2 - tk;
+                }
+                if (tk == nseg + W - p.n_own - 1) atomicExch(p.sched + 1, 0);
+            } else if (idx >= 0 && unit_w() < nseg) {
+                idx = -1;                           // this unit's own segment, once
+                return -2 - unit_w();
+            }
+            set_phase(2);
+        }
+        return -1;
+    }
+    // SR_SCHED: publish ring slot `pub` (= k + ahead) with decision v
+    __device__ void publish(int v) {
+        const int pub = k + ((st >> 5) & 1);
         const uint32_t s = (uint32_t)(pub % kSchedDepth);
         const uint32_t ph = (uint32_t)(pub / kSchedDepth) & 1u;
-        const bool pair = (role & 4) != 0;
         ptx::mbar_wait_u32(ring + kRingEmpty + 8u * s, ph ^ 1u);
-        const int W = (int)gridDim.x / (pair ? 2 : 1);
-        const int g = tk < p.n_whole ? tk : -1;
-        // every unit draws exactly one failing ticket; the last one drawn
-        // (n_whole + W - 1) resets the counter for the next launch
-        if (tk == p.n_whole + W - 1) atomicExch(p.sched, 0);
-        ptx::st_shared_u32(ring + kRingSlot + 4u * s, (uint32_t)g);
-        if (pair) {
+        ptx::st_shared_u32(ring + kRingSlot + 4u * s, (uint32_t)v);
+        if (st & 4) {
             // the peer's copy: an asynchronous remote store completing 4 bytes
             // of transaction on the peer's full[s] (armed by the relaxed
             // expect_tx arrival): the scheduler never waits on the DSMEM trip
             const uint32_t pbar = ptx::mapa_shared(ring + kRingFull + 8u * s, 1);
             ptx::mbar_arrive_expect_tx_cluster_relaxed(pbar, 4u);
-            ptx::st_async_u32(ptx::mapa_shared(ring + kRingSlot + 4u * s, 1), (uint32_t)g, pbar);
+            ptx::st_async_u32(ptx::mapa_shared(ring + kRingSlot + 4u * s, 1), (uint32_t)v, pbar);
         }
         ptx::mbar_arrive_u32(ring + kRingFull + 8u * s);
-        ++pub;
-        return g;
+        st |= 1 << 5;                               // one ahead of k (or at k, filled)
+        if (v == -1) set_phase(3);                  // the end is published
     }
-    // SR_SCHED: publish the ring one unit ahead of its own position (the
-    // peer CTA and the consumers learn the next group early) and keep the
-    // ticket after that drawn (its L2 round trip overlaps a unit of loads).
-    // Called by the producer once the current unit's first loads are issued,
-    // so the handshake stays off the critical path.
+    // SR_SCHED: publish the ring one decision ahead of its own position (the
+    // peer CTA and the consumers learn the next group early) and, for drawn
+    // whole groups, keep the ticket after that drawn (its L2 round trip
+    // overlaps a unit of loads).  Called by the producer once the current
+    // unit's first loads are issued, so the handshake stays off the critical
+    // path.
     __device__ void advance() {
-        if (!DYN || !ring || (role & 3) != SR_SCHED) return;
-        while (pub <= k && pend != -2) {
-            const int tk = pend >= 0 ? pend : atomicAdd(p.sched, 1);
-            pend = -1;
-            if (publish(tk) < 0) pend = -2;
-        }
-        if (pend == -1) pend = atomicAdd(p.sched, 1);
+        if (!DYN || (st & 3) != SR_SCHED) return;
+        if (!((st >> 5) & 1) && phase() != 3) publish(decide());
+        if (phase() == 0 && p.dyn && pend == -1) pend = atomicAdd(p.sched, 1);
     }
-    // next dynamic group; -1 = over.  Warps call this with all lanes; lane 0
-    // (or the single producer lane) does the arrivals, relaxed: the slot value
-    // is already in a register.
-    __device__ int dyn_next(bool single_thread) {
+    // the k-th decision.  Warps call this with all lanes; lane 0 (or the
+    // single producer lane) does the arrivals, relaxed: the slot value is
+    // already in a register.
+    __device__ int ring_next(bool single_thread) {
         const uint32_t s = (uint32_t)(k % kSchedDepth);
         const uint32_t ph = (uint32_t)(k / kSchedDepth) & 1u;
-        int g;
-        if ((role & 3) == SR_SCHED) {
-            while (pub <= k && pend != -2) {        // (first unit, or advance() not called)
-                const int tk = pend >= 0 ? pend : atomicAdd(p.sched, 1);
-                pend = -1;
-                if (publish(tk) < 0) pend = -2;
+        int v;
+        if ((st & 3) == SR_SCHED) {
+            if (!((st >> 5) & 1)) {                 // slot k not published yet
+                st &= ~(1 << 5);
+                publish(decide());
             }
-            g = (int)ptx::ld_shared_u32(ring + kRingSlot + 4u * s);
+            st &= ~(1 << 5);                        // after ++k: slot k+1 not yet published
+            v = (int)ptx::ld_shared_u32(ring + kRingSlot + 4u * s);
         } else {
-            const bool peer = (role & 3) == SR_PEER;
+            const bool peer = (st & 3) == SR_PEER;
             if (peer) ptx::mbar_wait_cluster_u32(ring + kRingFull + 8u * s, ph);
             else ptx::mbar_wait_u32(ring + kRingFull + 8u * s, ph);
-            g = (int)ptx::ld_shared_u32(ring + kRingSlot + 4u * s);
+            v = (int)ptx::ld_shared_u32(ring + kRingSlot + 4u * s);
             if (!single_thread) __syncwarp();
             if (single_thread || ptx::lane_id() == 0) {
                 if (peer) ptx::mbar_arrive_cluster_relaxed(ptx::mapa_shared(ring + kRingEmpty + 8u * s, 0));
@@ -287,47 +333,59 @@ struct UnitIter {
             }
         }
         ++k;
-        return g;
+        return v;
     }
     __device__ bool next(Unit& u, bool single_thread = false) {
-        if (DYN && ring) {
-            const int g = dyn_next(single_thread);
-            if (g >= 0) {
-                u.g = g;
-                u.r0 = 0;
-                u.r1 = p.R;
-                u.role = ROLE_WHOLE;
+        for (;;) {
+            const int t_end = seg >= 0 ? seg_end() : 0;
+            if (t < t_end) {                       // units of the current tail segment
+                int gl = t / p.R;                  // tail-local group
+                int r0 = (int)(t - gl * p.R);
+                int stop = (gl + 1) * p.R;
+                if (stop > t_end) stop = t_end;
+                int r1 = (int)(stop - gl * p.R);
+                u.g = p.n_whole + (int)gl;
+                u.r0 = r0;
+                u.r1 = r1;
+                u.role = (r0 == 0 && r1 == p.R) ? ROLE_WHOLE : (r0 == 0 ? ROLE_OWNER : ROLE_CONTRIB);
                 u.rev = 0;
+                u.seg = seg;
+                t = stop;
                 return true;
             }
-            ring = 0u;          // dynamic phase over: the static tail follows
+            if constexpr (DYN) {
+                const int v = ring_next(single_thread);
+                if (v >= 0) {
+                    u.g = v;
+                    u.r0 = 0;
+                    u.r1 = p.R;
+                    u.role = ROLE_WHOLE;
+                    u.rev = 0;
+                    u.seg = -1;
+                    return true;
+                }
+                if (v == -1) return false;
+                seg = -2 - v;
+                t = seg_begin(seg);
+                continue;
+            } else {
+                if (idx < p.q) {
+                    const int w = unit_w();
+                    u.g = idx * p.W + w;
+                    if (u.g >= p.G) return false;  // schedule 3: last round of whole groups
+                    u.r0 = 0;
+                    u.r1 = p.R;
+                    u.role = ROLE_WHOLE;
+                    // serpentine product order over rounds: a round starts with the
+                    // product the previous round ended with
+                    u.rev = p.serpentine ? (idx & 1) : 0;
+                    u.seg = -1;
+                    ++idx;
+                    return true;
+                }
+                return false;
+            }
         }
-        if (idx < p.q) {
-            u.g = idx * p.W + w;
-            if (u.g >= p.G) return false;      // schedule 3: last round of whole groups
-            u.r0 = 0;
-            u.r1 = p.R;
-            u.role = ROLE_WHOLE;
-            // serpentine product order over rounds: a round starts with the
-            // product the previous round ended with (its operand panels are
-            // still in L2)
-            u.rev = p.serpentine ? (idx & 1) : 0;
-            ++idx;
-            return true;
-        }
-        if (t >= t_end) return false;
-        int gl = t / p.R;                // tail-local group
-        int r0 = (int)(t - gl * p.R);
-        int stop = (gl + 1) * p.R;
-        if (stop > t_end) stop = t_end;
-        int r1 = (int)(stop - gl * p.R);
-        u.g = p.n_whole + (int)gl;
-        u.r0 = r0;
-        u.r1 = r1;
-        u.role = (r0 == 0 && r1 == p.R) ? ROLE_WHOLE : (r0 == 0 ? ROLE_OWNER : ROLE_CONTRIB);
-        u.rev = 0;
-        t = stop;
-        return true;
     }
 };
 
@@ -858,7 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool bf16 = ((p.idesc >> 7) & 7u) == 1u;   // kind::f16 a_format: 1 = bf16, 0 = fp16
             int stage = 0;
             uint32_t phase = 0;
-            UnitIter<false> it(p, w);
+            UnitIter<false> it(p, w, 0u, SR_LOCAL, CG);
             Unit u;
             while (it.next(u)) {
                 for (int t = u.r0; t < u.r1; ++t) {
@@ -943,7 +1001,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long brow = (long long)x * C_::kTileM + (long long)rank * kBM + row;
             // C_ij already touched inside this unit (bit ij): first contribution test
             uint32_t seen = 0;
-            const int slot = (u.role == ROLE_CONTRIB) ? (int)gridDim.x + (int)blockIdx.x : (int)blockIdx.x;
+            // split segments: a contributor's partials live in its segment's slot
+            // (the owner reads them after this pair may have moved on)
+            const int slot = (u.role == ROLE_CONTRIB) ? (int)gridDim.x + u.seg * CG + (int)rank : (int)blockIdx.x;
             const bool whole = u.role == ROLE_WHOLE;
             for (int t = u.r0; t < u.r1; ++t) {
                 const int r = product_at(p, u, t);
@@ -1146,16 +1206,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __threadfence();
                 asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
                 if (ew == 0 && lane == 0) {
-                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flags + blockIdx.x), "r"(1)
+                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flags + u.seg * CG + (int)rank), "r"(1)
                                  : "memory");
                 }
                 continue;
             }
-            // owner: the other segments live on work units w+1 .. last (same rank)
+            // owner: the other segments of the group are segments seg+1 .. last
+            // (same rank); static tail: segment == work unit
             const long long Tt_base = (long long)(u.g - p.n_whole) * p.R;   // tail-local first tile
             const int last_w = (int)((Tt_base + p.R - 1) / p.tail_c);
             if (ew == 0 && lane == 0) {
-                for (int v = w + 1; v <= last_w; ++v) {
+                for (int v = u.seg + 1; v <= last_w; ++v) {
                     int f = 0;
                     do {
                         asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.flags + v * CG + rank)
@@ -1175,7 +1236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // units w+1 .. last_w whose positions contribute to C_ij (bit d of
                 // cm[] = unit w+1+d; last_w - w < R <= kMaxR = 128)
                 uint64_t cm[2] = {0ull, 0ull};
-                for (int vw = w + 1; vw <= last_w; ++vw) {
+                for (int vw = u.seg + 1; vw <= last_w; ++vw) {
                     int lo = (int)((long long)vw * p.tail_c - Tt_base);
                     int hi = lo + p.tail_c;
                     if (lo < 0) lo = 0;
@@ -1183,7 +1244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     bool contributes = false;
                     for (int t = lo; t < hi; ++t)
                         if (p.Wc[p.rperm[t] * mn + ij]) { contributes = true; break; }
-                    const int d = vw - w - 1;
+                    const int d = vw - u.seg - 1;
                     if (contributes) cm[d >> 6] |= 1ull << (d & 63);
                 }
                 const bool own = (seen >> ij) & 1u;
@@ -1208,7 +1269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             } else if (m0 | m1) {
                                 const int d = m0 ? __ffsll((long long)m0) - 1 : 64 + __ffsll((long long)m1) - 1;
                                 if (d < 64) m0 &= m0 - 1; else m1 &= m1 - 1;
-                                sl = (int)gridDim.x + (w + 1 + d) * CG + (int)rank;
+                                sl = (int)gridDim.x + (u.seg + 1 + d) * CG + (int)rank;
                             }
                             src[q] = sl;
                             ns += sl >= 0;
@@ -1243,7 +1304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // all reads done -> reset the flags for the next launch
             asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
             if (ew == 0 && lane == 0)
-                for (int v = w + 1; v <= last_w; ++v) p.flags[v * CG + rank] = 0;
+                for (int v = u.seg + 1; v <= last_w; ++v) p.flags[v * CG + rank] = 0;
         }
         if (p.stats && ew == 0 && lane == 0) {
             p.stats[blockIdx.x * kStatsPerCta + 4] = w_tfull;

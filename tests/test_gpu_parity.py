@@ -411,13 +411,14 @@ def test_partial_homes_exact_diag_build():
     assert "homes ok" in r.stdout
 
 
-@pytest.mark.parametrize("schedule", [1, 5])
+@pytest.mark.parametrize("schedule", [1, 5, 6])
 @pytest.mark.parametrize("algo,shape,ctas", [("strassen", (1536, 2304, 512), 0), ("strassen", (1536, 2304, 512), 10),
                                              ("strassen", (2560, 3072, 256), 6), ("laderman", (1000, 808, 520), 4),
                                              ("classical", (2304, 2560, 256), 8), ("classical", (1000, 1048, 520), 0)])
 def test_dynamic_vs_static_schedule_exact(schedule, algo, shape, ctas):
-    # schedule 5: whole groups drawn from the workspace ticket counter at run
-    # time; 1 (default): the static lockstep assignment.  Exact both
+    # schedule 5: whole groups and split-tail segments drawn from the workspace
+    # ticket counters at run time; 6: static whole groups, run-time tail;
+    # 1 (default): the static lockstep assignment.  Exact every
     # ways; repeated calls on one workspace check that the counter is back at
     # zero after every launch (a stale counter would skip or repeat groups)
     plan = _exact_case(*shape, algo, schedule=schedule, num_ctas=ctas)
@@ -428,7 +429,7 @@ def test_dynamic_vs_static_schedule_exact(schedule, algo, shape, ctas):
     C1 = plan.gemm(A, B, workspace=ws).clone()
     for _ in range(4):
         assert torch.equal(plan.gemm(A, B, workspace=ws), C1)
-    assert int(ws[:4].view(torch.int32)[0]) == 0          # counter reset by the last ticket
+    assert ws[:8].view(torch.int32).tolist() == [0, 0]      # counters reset by the last tickets
 
 
 @pytest.mark.parametrize("b_layout", [0, 1])
