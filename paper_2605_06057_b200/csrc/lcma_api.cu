@@ -103,6 +103,7 @@ struct lcma_plan_s {
     int nX, nZ, G, nK;
     int ctas, cg, bn, q, tail_c, swz;
     int n_whole, dyn, dyn_tail;
+    int nbatch = 1;                // batched inner GEMMs of a two-level plan (groups = nbatch x nX x nZ)
     size_t off_sched, off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
     size_t off_inner = 0;          // two-level: the inner plan's partial slots + flags
     lcma_plan_s* inner = nullptr;  // two-level: fused GEMM plan of the base scheme
@@ -379,6 +380,13 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             delete p;
             return fail(LCMA_ERR_NOT_SUPPORTED, "two-level: inner block extents differ");
         }
+        // the R0 inner GEMMs (one per outer product q) run as ONE batched
+        // launch over R0 x nX x nZ groups: one split tail instead of R0, and
+        // enough groups per launch for the persistent grid
+        in->nbatch = B0.R;
+        in->G = in->nX * in->nZ * in->nbatch;
+        make_schedule(in, (d.schedule >= 2 && d.schedule <= 6) ? d.schedule : 1);
+        if ((in->dyn || in->dyn_tail) && (in->cg != 2 || in->bn != 256)) make_schedule(in, 1);
         p->inner = in;
     }
 
@@ -825,18 +833,18 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     CUtensorMap ta, tb;
     // A operand: K-major rows (PF: the raw A, its blocks are combined in the kernel)
     const uint64_t a_cols = (classical || pf) ? p->d.K : p->Kb;
-    const uint64_t a_rows = (classical || pf) ? p->d.M : (uint64_t)S.R * p->Mb;
+    const uint64_t a_rows = (classical || pf) ? p->d.M : (uint64_t)S.R * p->Mb * p->nbatch;
     rs = make_map(&ta, Aop, dt, a_cols, a_rows, epr, kBM);
     if (rs != LCMA_OK) return rs;
     const bool b_mn = p->d.b_layout == 0;
     bool b3d = false;
     if (!b_mn) {   // N x K (K-major); PF 2: the raw B, its blocks are combined in the kernel
         const uint64_t cols = (classical || pf == 2) ? p->d.K : p->Kb;
-        const uint64_t rows = (classical || pf == 2) ? p->d.N : (uint64_t)S.R * p->Nb;
+        const uint64_t rows = (classical || pf == 2) ? p->d.N : (uint64_t)S.R * p->Nb * p->nbatch;
         rs = make_map(&tb, Bop, dt, cols, rows, epr, p->bn / p->cg);
     } else {       // K x N (MN-major): boxes of 128 bytes of N x BK rows
         const uint64_t cols = classical ? p->d.N : p->Nb;
-        const uint64_t rows = classical ? p->d.K : (uint64_t)S.R * p->Kb;
+        const uint64_t rows = classical ? p->d.K : (uint64_t)S.R * p->Kb * p->nbatch;
         CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
         if (dt == LCMA_TF32 || dt == LCMA_FP32) {
             if (const char* v = diag_env("LCMA_TF32_MN_SWZ")) swz = (CUtensorMapSwizzle)std::atoi(v);
@@ -852,6 +860,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     GemmParams g;
     std::memset(&g, 0, sizeof(g));
     g.nX = p->nX; g.nZ = p->nZ; g.G = p->G; g.R = S.R; g.nK = p->nK; g.BK = p->BK;
+    g.nbatch = p->nbatch;
+    g.Gb = p->nX * p->nZ;
     g.a_rows_per_r = classical ? 0 : (int)p->Mb;
     g.b_rows_per_r = classical ? 0 : (int)(b_mn ? p->Kb : p->Nb);
     g.b_mn_major = b_mn;
@@ -1142,16 +1152,10 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
         float* Pi = reinterpret_cast<float*>(w + p->off_inner + in->off_P);
         int* Fi = reinterpret_cast<int*>(w + p->off_inner + in->off_flags);
         int* Si = reinterpret_cast<int*>(w + p->off_inner + in->off_sched);
-        // the measurement events bracket all inner GEMMs together
-        cudaEvent_t ev0 = t_ev_start, ev1 = t_ev_end;
-        t_ev_start = t_ev_end = nullptr;
-        if (ev0) cudaEventRecord(ev0, st);
-        for (int q = 0; q < B0.R && rs == LCMA_OK; ++q)
-            rs = launch_umma(in, static_cast<const uint8_t*>(At) + q * a_slice,
-                             static_cast<const uint8_t*>(Bt) + q * b_slice, H + q * h_slice, Pi, Fi, Si, nullptr, st);
-        if (ev1) cudaEventRecord(ev1, st);
-        t_ev_start = ev0;
-        t_ev_end = ev1;
+        // all R0 inner GEMMs in one batched launch: batch q reads the slices
+        // At[q*R0 .. q*R0+R0-1], Bt[...] and writes H_q = H + q * h_slice
+        (void)a_slice; (void)b_slice; (void)h_slice;
+        rs = launch_umma(in, At, Bt, H, Pi, Fi, Si, nullptr, st);
         if (rs != LCMA_OK) return rs;
         return launch_combine_h_ex(p, B0, B0.m * p->Mb, B0.n * p->Nb, H, C, st);
     }

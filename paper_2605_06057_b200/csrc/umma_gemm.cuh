@@ -129,6 +129,12 @@ struct GemmParams {
     int* sched;            // dyn / dyn_tail: ticket counters [2] (workspace, zero between launches)
     int dyn_tail;          // 1: tail segments handed out at run time (DYN instantiation)
     int n_own;             // split groups of the tail (= owner segments)
+    // batched GEMMs (two-level schemes: the R0 inner fused GEMMs of the outer
+    // products in one launch): group g -> batch q = g / Gb, in-batch group
+    // g % Gb; batch q's products are operand-map products r + q * R (the
+    // composed index 7q + r2 of reading 3) and it writes C rows + q * M
+    // (C = [nbatch][M][ldc])
+    int nbatch, Gb;
     // epilogue
     int epi_mode;
     int out_type;
@@ -398,6 +404,7 @@ __device__ __forceinline__ int product_at(const GemmParams& p, const Unit& u, in
 // column by column so that the W groups of a lockstep round cover a compact
 // (x, z) region (operand reuse in L2).
 __device__ __forceinline__ void group_xz(const GemmParams& p, int g, int& x, int& z) {
+    if (p.nbatch > 1) g %= p.Gb;
     int band_tiles = p.swz * p.nZ;
     int band = g / band_tiles;
     int within = g - band * band_tiles;
@@ -496,8 +503,9 @@ __device__ __forceinline__ void store_c_row(const GemmParams& p, long long row, 
 // epilogue work in 16-column halves so that only 16 temporaries are live
 // next to the register partial (fewer spills).
 __device__ __forceinline__ void store_c_row16(const GemmParams& p, long long row, long long c0,
-                                              const float* v) {
+                                              const float* v, long long radd = 0) {
     if (row >= p.M) return;
+    row += radd;                                   // batched GEMMs: batch q's rows start at q * M
     if (p.debug & 2048) {
         // diagnostics (results WRONG): the same bytes, fully coalesced -- the
         // 32 lanes of a warp write 1 KB contiguous of one row band
@@ -707,8 +715,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             while (it.next(u, true)) {
                 int x, z;
                 group_xz(p, u.g, x, z);
+                const int qb = p.nbatch > 1 ? u.g / p.Gb : 0;
                 for (int t = u.r0; t < u.r1; ++t) {
-                    const int r = product_at(p, u, t);
+                    // (batched: the batch's products are rows r + qb * R of the maps)
+                    const int r = product_at(p, u, t) + qb * p.R;
                     const int a_row = r * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
                     const int b_col0 = z * BN + (int)rank * C_::kBNc;
                     for (int kb = 0; kb < p.nK; ++kb) {
@@ -997,6 +1007,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (it.next(u)) {
             int x, z;
             group_xz(p, u.g, x, z);
+            const long long radd = p.nbatch > 1 ? (long long)(u.g / p.Gb) * p.M : 0;   // batch's C rows
             // rows of this CTA inside the block grid
             const long long brow = (long long)x * C_::kTileM + (long long)rank * kBM + row;
             // C_ij already touched inside this unit (bit ij): first contribution test
@@ -1084,8 +1095,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     for (int e = 0; e < 32; ++e)
                                         pr[e] = (first ? 0.f : pr[e]) + sw * __uint_as_float(raw[e]);
                                     if (in_range && !(p.debug & 128)) {
-                                        store_c_row16(p, (long long)i * p.Mb + brow, ccol, pr);
-                                        store_c_row16(p, (long long)i * p.Mb + brow, ccol + 16, pr + 16);
+                                        store_c_row16(p, (long long)i * p.Mb + brow, ccol, pr, radd);
+                                        store_c_row16(p, (long long)i * p.Mb + brow, ccol + 16, pr + 16, radd);
                                     }
                                 } else if (first) {
 #pragma unroll
@@ -1113,7 +1124,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             v[e + 3] = o.w + sw * __uint_as_float(raw[hh + e + 3]);
                                         }
                                         if (in_range && !(p.debug & 128))
-                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v);
+                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v, radd);
                                     }
                                 } else {
 #pragma unroll
@@ -1151,7 +1162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             }
                                         }
                                         if (in_range && !(p.debug & 128))
-                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v);
+                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v, radd);
                                     }
                                     if (!first && p.discard) {
                                         __syncwarp();      // the 8 lanes sharing a line have read it
@@ -1298,7 +1309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     const long long ccol = (long long)j * p.Nb + (long long)z * BN + col0;
                     if (brow < p.Mb && ccol < (long long)(j + 1) * p.Nb)
-                        store_c_row16(p, (long long)i * p.Mb + brow, ccol, v);
+                        store_c_row16(p, (long long)i * p.Mb + brow, ccol, v, radd);
                 }
             }
             // all reads done -> reset the flags for the next launch
