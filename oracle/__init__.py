@@ -707,3 +707,135 @@ def freivalds(C, A, B, trials=4, seed=0) -> float:
         r = C @ x - A @ (B @ x)
         worst = max(worst, float(np.linalg.norm(r) / (nA * nB * np.linalg.norm(x))))
     return worst
+
+
+# ================================================================ FP8
+# "the full BF16-to-quantized-FP8 workflow with 1 x 128 block-wise scaling for
+# FP8E4M3", "fuses the quantization into the Combine A stage".
+# DESIGN.md reading 23: every 1 x 128 block (one row of an operand, 128
+# consecutive K elements) gets one power-of-two scale 2^e (UE8M0), the smallest
+# with amax <= 448 * 2^e; the block is stored as E4M3(x / 2^e) (RN-even,
+# satfinite).  B~ blocks run along K for each output column.  The oracle
+# quantizes the exact (fp64) combined operand; the product and Combine H are
+# exact (fp64), C is rounded once to the output type.
+E4M3_MAX = 448.0
+
+
+def round_e4m3(x) -> np.ndarray:
+    """RN-even rounding of fp64 values to FP8 E4M3 (OCP E4M3: bias 7, 3
+    mantissa bits, normals 2^-6 .. 448, subnormal spacing 2^-9, no
+    infinities), saturating to +-448."""
+    x = np.asarray(x, np.float64)
+    a = np.abs(x)
+    _, ex = np.frexp(np.where(a > 0, a, 1.0))      # a = f * 2^ex, f in [0.5, 1)
+    e = np.maximum(ex - 1, -6)                      # binade exponent (subnormals share -6)
+    spacing = np.ldexp(1.0, e - 3)                  # 3 mantissa bits
+    y = np.round(a / spacing) * spacing             # np.round: half to even
+    y = np.minimum(y, E4M3_MAX)
+    return np.where(x < 0, -y, y)
+
+
+def scale_exponent(amax) -> np.ndarray:
+    """Smallest integer e with amax <= 448 * 2^e (0 for an all-zero block),
+    clamped to the UE8M0 range [-127, 127].  Written as the definition: a
+    first guess from log2, then exact comparisons move it to the minimum."""
+    amax = np.asarray(amax, np.float64)
+    pos = amax > 0
+    safe = np.where(pos, amax, E4M3_MAX)
+    e = np.ceil(np.log2(safe / E4M3_MAX)).astype(np.int64)
+    for _ in range(2):
+        e = np.where(safe > np.ldexp(E4M3_MAX, e), e + 1, e)            # not enough
+        e = np.where(safe <= np.ldexp(E4M3_MAX, e - 1), e - 1, e)       # not the smallest
+    e = np.where(pos, e, 0)
+    return np.clip(e, -127, 127)
+
+
+def quantize_1x128(X):
+    """1 x 128 block scaling of a (rows, K) operand, K a multiple of 128:
+    returns (Q, e) with Q the E4M3 values (as fp64) and e[rows, K/128] the
+    scale exponents; the dequantized operand is Q * 2^e per block."""
+    X = np.asarray(X, np.float64)
+    rows, K = X.shape
+    if K % 128:
+        raise ValueError("K must be a multiple of 128 (zero-pad the block)")
+    blk = X.reshape(rows, K // 128, 128)
+    e = scale_exponent(np.abs(blk).max(axis=2))
+    Q = round_e4m3(blk / np.ldexp(1.0, e)[..., None])
+    return Q.reshape(rows, K), e
+
+
+def dequantize_1x128(Q, e) -> np.ndarray:
+    Q = np.asarray(Q, np.float64)
+    rows, K = Q.shape
+    return (Q.reshape(rows, K // 128, 128) * np.ldexp(1.0, np.asarray(e))[..., None]).reshape(rows, K)
+
+
+def combine_b_fp8(B, s: Scheme, extents):
+    """Combine B (Eq. 4) in exact arithmetic, then each B~_r quantized
+    1 x 128 along K per column n (reading 23).  Returns (Q[R][Nb][Kb],
+    e[R][Nb][Kb/128]) -- B~_r stored N x K, the nn.Linear layout."""
+    B = np.asarray(B, np.float64)
+    K, N = B.shape
+    Mb, Kb, Nb = extents
+    Bp = np.zeros((s.k * Kb, s.n * Nb))
+    Bp[:K, :N] = B
+    Q = np.empty((s.R, Nb, Kb))
+    E = np.empty((s.R, Nb, Kb // 128), np.int64)
+    for r in range(s.R):
+        acc = np.zeros((Kb, Nb))
+        for l in range(s.k):
+            for j in range(s.n):
+                if s.V[r, l, j]:
+                    acc += s.V[r, l, j] * Bp[l * Kb:(l + 1) * Kb, j * Nb:(j + 1) * Nb]
+        Q[r], E[r] = quantize_1x128(acc.T)
+    return Q, E
+
+
+def combine_a_fp8_rows(A, s: Scheme, rows_x, extents):
+    """Combine A (Eq. 3) for block rows x in `rows_x`, exact, then 1 x
+    128 quantization along K (the quantization fused into Combine A).
+    Returns (Q[R][len(rows_x)][Kb], e[R][len(rows_x)][Kb/128])."""
+    A = np.asarray(A, np.float64)
+    M, K = A.shape
+    Mb, Kb, Nb = extents
+    Ap = np.zeros((s.m * Mb, s.k * Kb))
+    Ap[:M, :K] = A
+    xs = np.asarray(rows_x, np.int64)
+    Q = np.empty((s.R, len(xs), Kb))
+    E = np.empty((s.R, len(xs), Kb // 128), np.int64)
+    for r in range(s.R):
+        acc = np.zeros((len(xs), Kb))
+        for i in range(s.m):
+            for l in range(s.k):
+                if s.U[r, i, l]:
+                    acc += s.U[r, i, l] * Ap[i * Mb + xs, l * Kb:(l + 1) * Kb]
+        Q[r], E[r] = quantize_1x128(acc)
+    return Q, E
+
+
+def lcma_rows_fp8(A, B, s: Scheme, rows, extents, fmt_out=None, bq=None) -> np.ndarray:
+    """Rows `rows` of Algorithm 1 on the FP8 path: Combine A / B
+    exact then quantized 1 x 128 (reading 23), H_r = dequant(A~_r) .
+    dequant(B~_r) exact (Eq. 5; a library matmul step), Combine H (Eq. 6)
+    exact, C rounded once to fmt_out.  `bq` = a precomputed combine_b_fp8."""
+    A = np.asarray(A, np.float64)
+    M, K = A.shape
+    N = np.asarray(B).shape[1]
+    Mb, Kb, Nb = extents
+    QB, EB = bq if bq is not None else combine_b_fp8(B, s, extents)
+    Bdq = [dequantize_1x128(QB[r], EB[r]).T for r in range(s.R)]          # Kb x Nb
+    rows = np.asarray(rows, np.int64)
+    out = np.zeros((len(rows), N))
+    for q, rho in enumerate(rows):
+        i, x = divmod(int(rho), Mb)
+        QA, EA = combine_a_fp8_rows(A, s, [x], extents)
+        crow = np.zeros(s.n * Nb)
+        for r in range(s.R):
+            if not s.W[r, i, :].any():
+                continue
+            h = dequantize_1x128(QA[r], EA[r])[0] @ Bdq[r]                 # Eq. 5, row x of H_r
+            for j in range(s.n):                                            # Eq. 6
+                if s.W[r, i, j]:
+                    crow[j * Nb:(j + 1) * Nb] += s.W[r, i, j] * h
+        out[q] = crow[:N]
+    return round_to(out, fmt_out) if fmt_out else out
