@@ -61,7 +61,14 @@ typedef enum {
     LCMA_BF16 = 0,   /* bf16 storage, bf16 MMA, fp32 accumulation                  */
     LCMA_FP16 = 1,   /* fp16 storage, fp16 MMA, fp32 accumulation                  */
     LCMA_TF32 = 2,   /* fp32 storage, tf32 MMA (RN-away rounding of combined terms) */
-    LCMA_FP32 = 3    /* fp32 storage, true fp32 SIMT arithmetic                     */
+    LCMA_FP32 = 3,   /* fp32 storage, true fp32 SIMT arithmetic                     */
+    LCMA_FP8_E4M3 = 4 /* bf16 A and B in, FP8 E4M3 MMA: the combines quantize
+                        every 1 x 128 block (one row, 128 consecutive K) of A~_r and
+                        B~_r with a power-of-two UE8M0 scale (quantization fused into
+                        Combine A; reading 23); block-scaled
+                        tcgen05 MMA, fp32 accumulation; C bf16 (out_dtype BF16 or
+                        FP8_E4M3) or fp32.  B must be N x K (b_layout 1).  The
+                        classical plan quantizes A (and B) with the same pass.     */
 } lcma_dtype;
 
 typedef enum {
@@ -170,10 +177,19 @@ lcma_status lcma_btilde_size(lcma_plan_t plan, size_t* bytes);
 lcma_status lcma_gemm(lcma_plan_t plan, const void* A, const void* B, void* C,
                       void* workspace, size_t workspace_bytes, void* cuda_stream);
 
+/* Byte offset of a workspace region (which 0: A~, 1: B~ combined per call;
+ * LCMA_FP8_E4M3: the E4M3 operand followed by its UE8M0 scale chunks).  For
+ * tests and tools that read the materialised combines back; INVALID_VALUE
+ * for a plan without such a region (a classical bf16/fp16/tf32 plan). */
+lcma_status lcma_workspace_region(lcma_plan_t plan, int32_t which, size_t* offset);
+
 /* Offline Combine B for static weights: Bt = group-combined
  * B for this plan's scheme and extents (lcma_btilde_size bytes).  Bt is bound
  * to the plan's (N, K, dtype, scheme, extents, b_layout); lcma_gemm_precombined
- * trusts the caller to pass a matching Bt. */
+ * trusts the caller to pass a matching Bt.  LCMA_FP8_E4M3: Bt holds the
+ * quantized B~ (E4M3 [R][Nb][Kb]) followed by its UE8M0 scale chunks
+ * ([R][Nb/128][Kb/128] x 512 bytes, the tcgen05 block-scale layout); the
+ * classical FP8 plan accepts it too (B quantized once, R = 1). */
 lcma_status lcma_precombine_b(lcma_plan_t plan, const void* B, void* Bt, void* cuda_stream);
 lcma_status lcma_gemm_precombined(lcma_plan_t plan, const void* A, const void* Bt, void* C,
                                   void* workspace, size_t workspace_bytes, void* cuda_stream);

@@ -791,15 +791,23 @@ def combine_b_fp8(B, s: Scheme, extents):
     return Q, E
 
 
+def _padded_rows(X, rows, c0, width):
+    """Rows `rows` of X, columns [c0, c0 + width), zero outside X."""
+    out = np.zeros((len(rows), width))
+    R_, C_ = X.shape
+    for q, rho in enumerate(rows):
+        if rho < R_ and c0 < C_:
+            seg = X[rho, c0:min(c0 + width, C_)]
+            out[q, :len(seg)] = seg
+    return out
+
+
 def combine_a_fp8_rows(A, s: Scheme, rows_x, extents):
     """Combine A (Eq. 3) for block rows x in `rows_x`, exact, then 1 x
     128 quantization along K (the quantization fused into Combine A).
     Returns (Q[R][len(rows_x)][Kb], e[R][len(rows_x)][Kb/128])."""
     A = np.asarray(A, np.float64)
-    M, K = A.shape
     Mb, Kb, Nb = extents
-    Ap = np.zeros((s.m * Mb, s.k * Kb))
-    Ap[:M, :K] = A
     xs = np.asarray(rows_x, np.int64)
     Q = np.empty((s.R, len(xs), Kb))
     E = np.empty((s.R, len(xs), Kb // 128), np.int64)
@@ -808,7 +816,7 @@ def combine_a_fp8_rows(A, s: Scheme, rows_x, extents):
         for i in range(s.m):
             for l in range(s.k):
                 if s.U[r, i, l]:
-                    acc += s.U[r, i, l] * Ap[i * Mb + xs, l * Kb:(l + 1) * Kb]
+                    acc += s.U[r, i, l] * _padded_rows(A, i * Mb + xs, l * Kb, Kb)
         Q[r], E[r] = quantize_1x128(acc)
     return Q, E
 
@@ -826,14 +834,16 @@ def lcma_rows_fp8(A, B, s: Scheme, rows, extents, fmt_out=None, bq=None) -> np.n
     Bdq = [dequantize_1x128(QB[r], EB[r]).T for r in range(s.R)]          # Kb x Nb
     rows = np.asarray(rows, np.int64)
     out = np.zeros((len(rows), N))
+    xs = np.unique(rows % Mb)
+    QA, EA = combine_a_fp8_rows(A, s, xs, extents)
     for q, rho in enumerate(rows):
         i, x = divmod(int(rho), Mb)
-        QA, EA = combine_a_fp8_rows(A, s, [x], extents)
+        k = int(np.searchsorted(xs, x))
         crow = np.zeros(s.n * Nb)
         for r in range(s.R):
             if not s.W[r, i, :].any():
                 continue
-            h = dequantize_1x128(QA[r], EA[r])[0] @ Bdq[r]                 # Eq. 5, row x of H_r
+            h = dequantize_1x128(QA[r, k:k + 1], EA[r, k:k + 1])[0] @ Bdq[r]   # Eq. 5, row x of H_r
             for j in range(s.n):                                            # Eq. 6
                 if s.W[r, i, j]:
                     crow[j * Nb:(j + 1) * Nb] += s.W[r, i, j] * h

@@ -11,13 +11,13 @@ import ctypes
 import os
 
 __all__ = ["lib", "Plan", "decide", "scheme_get", "scheme_register_file", "scheme_register",
-           "LcmaError", "BF16", "FP16", "TF32", "FP32", "ALGO", "VARIANT"]
+           "LcmaError", "BF16", "FP16", "TF32", "FP32", "FP8", "ALGO", "VARIANT"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # LCMA_LIB: an alternative build of the same library (tuning experiments)
 _LIB_PATH = os.environ.get("LCMA_LIB") or os.path.join(_HERE, "liblcma.so")
 
-BF16, FP16, TF32, FP32 = 0, 1, 2, 3
+BF16, FP16, TF32, FP32, FP8 = 0, 1, 2, 3, 4   # FP8: bf16 in, E4M3 1x128-scaled MMA
 ALGO = {"auto": 0, "classical": 1, "strassen": 2, "strassen2": 3, "laderman": 4, "scheme": 5}
 VARIANT = {"auto": 0, "unfused": 1, "fused_h": 2, "producer": 3, "two_level": 4}
 STATUS = {0: "LCMA_OK", 1: "LCMA_ERR_INVALID_VALUE", 2: "LCMA_ERR_NOT_SUPPORTED",
@@ -88,6 +88,7 @@ def lib():
     L.lcma_plan_get_info.argtypes = [P, ctypes.POINTER(PlanInfo)]
     L.lcma_workspace_size.argtypes = [P, ctypes.POINTER(SZ)]
     L.lcma_btilde_size.argtypes = [P, ctypes.POINTER(SZ)]
+    L.lcma_workspace_region.argtypes = [P, ctypes.c_int32, ctypes.POINTER(SZ)]
     L.lcma_gemm.argtypes = [P, P, P, P, P, SZ, P]
     L.lcma_precombine_b.argtypes = [P, P, P, P]
     L.lcma_gemm_precombined.argtypes = [P, P, P, P, P, SZ, P]
@@ -109,7 +110,7 @@ def lib():
     for name in ("lcma_plan", "lcma_plan_ex", "lcma_plan_get_info", "lcma_workspace_size",
                  "lcma_btilde_size", "lcma_gemm", "lcma_precombine_b", "lcma_gemm_precombined",
                  "lcma_decide", "lcma_scheme_register_file", "lcma_scheme_register",
-                 "lcma_scheme_get", "lcma_plan_schedule"):
+                 "lcma_scheme_get", "lcma_plan_schedule", "lcma_workspace_region"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -133,7 +134,8 @@ _DT_TORCH = None
 
 def _torch_dtype(code):
     import torch
-    return {BF16: torch.bfloat16, FP16: torch.float16, TF32: torch.float32, FP32: torch.float32}[code]
+    return {BF16: torch.bfloat16, FP16: torch.float16, TF32: torch.float32, FP32: torch.float32,
+            FP8: torch.bfloat16}[code]
 
 
 class Plan:
@@ -146,7 +148,7 @@ class Plan:
                  decision_model=0, raster_rows=0):
         L = lib()
         if out_dtype is None:
-            out_dtype = FP32 if dtype == TF32 else dtype
+            out_dtype = FP32 if dtype == TF32 else (BF16 if dtype == FP8 else dtype)
         self._hw = _profile(hw)
         d = PlanDesc(M, N, K, dtype, out_dtype, ALGO[algo] if isinstance(algo, str) else algo,
                      scheme_id, b_layout, int(b_static),
@@ -257,7 +259,7 @@ class Plan:
         if C is None:
             C = self.empty_c(A.device)
         ws = workspace if workspace is not None else self.workspace(A.device, stream)
-        if self.info["algo"] == ALGO["classical"]:
+        if self.info["algo"] == ALGO["classical"] and self.dtype != FP8:
             dev = self._check_args(A, Bt, None, C, ws)     # classical: Bt is B itself
         else:
             dev = self._check_args(A, None, Bt, C, ws)
@@ -266,6 +268,12 @@ class Plan:
                                                ws.data_ptr(), ws.numel() * ws.element_size(),
                                                self._stream(stream, dev)))
         return C
+
+    def workspace_region(self, which):
+        """Byte offset of the A~ (0) / B~ (1) region of the workspace."""
+        off = ctypes.c_size_t()
+        _check(lib().lcma_workspace_region(self._h, which, ctypes.byref(off)))
+        return off.value
 
     def schedule(self, cta):
         cap = 4096

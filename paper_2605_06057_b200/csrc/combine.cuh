@@ -7,6 +7,7 @@
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <stdint.h>
 
 namespace lcma {
@@ -211,6 +212,100 @@ __global__ void __launch_bounds__(256) group_combine_kernel(const __grid_constan
                 }
             }
             store_vec<VEC>(p, (long long)r * per_r + e0 * p.E1 + e1, acc);
+        }
+    }
+}
+
+// FP8 Group Combine with the quantization fused in (DESIGN.md
+// reading 23): out_r = sum_{p,q} coef[r][p][q] * src blocks (bf16 sources,
+// fp32 signed sum in coefficient order as above), then every 1 x 128 block
+// of an output row is scaled by 2^-e, e the smallest integer with amax <= 448 *
+// 2^e (UE8M0, clamped to [-127, 127]; 0 for an all-zero block), and stored as
+// E4M3 (RN-even, satfinite).  The scale bytes go to the tcgen05 block-scale
+// layout: per (r, 128-row block, 128-column block) a 512-byte chunk, byte
+// (row % 32) * 16 + (row % 128 / 32) * 4 + j = e + 127 for the four 32-column
+// scale slots j of the MMA (equal: one scale per 1 x 128 block).
+// 16 consecutive threads own one 128-column block of a row (8 columns each):
+// the amax is a 16-lane shuffle reduction.
+struct CombineQ8Params {
+    const uint16_t* src;      // bf16, rows x cols row-major
+    uint8_t* dst;             // E4M3 [R][E0][E1]
+    uint32_t* sf;             // scale chunks [R][E0/128][E1/128][128] words
+    long long rows, cols;     // true source extents (zero padding beyond)
+    long long E0, E1;         // block extents: E0 % 128 == 0, E1 % 128 == 0
+    int P, Q, R;
+    int8_t coef[kCombMaxR * kCombMaxPQ];   // coef[r][p*Q + q]
+};
+
+// smallest e with amax <= 448 * 2^e (amax >= 0, exact fp32)
+__device__ __forceinline__ int ue8m0_exponent(float amax) {
+    const uint32_t b = __float_as_uint(amax);
+    const int ef = (int)(b >> 23) & 0xFF;
+    if (b == 0u) return 0;
+    if (ef == 0) return -127;                           // subnormal amax: below 448 * 2^-127
+    int e = (ef - 127) - 8 + ((b & 0x7FFFFFu) > 0x600000u ? 1 : 0);   // 448 = 1.75 * 2^8
+    return e < -127 ? -127 : (e > 127 ? 127 : e);
+}
+
+template <int PQ>
+__global__ void __launch_bounds__(256) group_combine_q8_kernel(const __grid_constant__ CombineQ8Params p) {
+    const long long nvec = p.E0 * (p.E1 / 8);
+    const long long per_r = p.E0 * p.E1;
+    const long long nkb = p.E1 / 128;
+    const int lane = threadIdx.x & 31;
+    for (long long vi = blockIdx.x * (long long)blockDim.x + threadIdx.x; vi < nvec;
+         vi += (long long)gridDim.x * blockDim.x) {
+        const long long e0 = vi / (p.E1 / 8);
+        const long long e1 = (vi - e0 * (p.E1 / 8)) * 8;
+        uint4 src[PQ];
+#pragma unroll
+        for (int pq = 0; pq < PQ; ++pq) {
+            const int pi = pq / p.Q, qi = pq - (pq / p.Q) * p.Q;
+            const long long r = pi * p.E0 + e0, c = qi * p.E1 + e1;
+            src[pq] = (pq < p.P * p.Q && r < p.rows && c < p.cols)
+                          ? __ldcs(reinterpret_cast<const uint4*>(p.src + r * p.cols + c))
+                          : make_uint4(0, 0, 0, 0);
+        }
+        for (int r = 0; r < p.R; ++r) {
+            float acc[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+            for (int pq = 0; pq < PQ; ++pq) {
+                const int cf = p.coef[r * PQ + pq];
+                if (!cf) continue;
+                const uint32_t w[4] = {src[pq].x, src[pq].y, src[pq].z, src[pq].w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+                    if (cf > 0) { acc[2 * h] += f.x; acc[2 * h + 1] += f.y; }
+                    else { acc[2 * h] -= f.x; acc[2 * h + 1] -= f.y; }
+                }
+            }
+            float amax = 0.f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) amax = fmaxf(amax, fabsf(acc[e]));
+#pragma unroll
+            for (int o = 8; o >= 1; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            const int ex = ue8m0_exponent(amax);
+            // 2^-e exactly (e <= 126 keeps it a normal fp32; e = 127 needs amax > 2^135)
+            const float inv = __uint_as_float((uint32_t)(127 - (ex > 126 ? 126 : ex)) << 23);
+            uint32_t q[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+                    make_float2(acc[4 * h] * inv, acc[4 * h + 1] * inv), __NV_SATFINITE, __NV_E4M3);
+                const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+                    make_float2(acc[4 * h + 2] * inv, acc[4 * h + 3] * inv), __NV_SATFINITE, __NV_E4M3);
+                q[h] = (uint32_t)lo | ((uint32_t)hi << 16);
+            }
+            __stcs(reinterpret_cast<uint2*>(p.dst + (long long)r * per_r + e0 * p.E1 + e1), make_uint2(q[0], q[1]));
+            if ((lane & 15) == 0) {
+                const uint32_t byte = (uint32_t)(ex + 127);
+                const long long chunk = ((long long)r * (p.E0 / 128) + e0 / 128) * nkb + e1 / 128;
+                const int rw = (int)(e0 & 127);
+                p.sf[chunk * 128 + (rw & 31) * 4 + (rw >> 5)] = byte * 0x01010101u;
+            }
         }
     }
 }

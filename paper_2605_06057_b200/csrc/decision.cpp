@@ -165,9 +165,11 @@ Profile default_profile(int dtype) {
     // 1.39 PFLOP/s under the power cap, HBM copy 6.55 TB/s; FLOPS_+ = fp32
     // FADD issue rate 148 SMs x 128 lanes x ~1.3 GHz sustained.
     Profile p;
-    const double bytes = (dtype == 0 || dtype == 1) ? 2.0 : 4.0;
-    // classical tcgen05 kernel of this build, cfg2 (profiles/): 1.366 PF/s bf16
-    p.flops_mul = dtype <= 1 ? 1.366e15 : (dtype == 2 ? 0.66e15 : 60e12);
+    // dtype 4 (FP8 E4M3): 1-byte operands after the quantizing combines
+    const double bytes = (dtype == 0 || dtype == 1) ? 2.0 : dtype == 4 ? 1.0 : 4.0;
+    // classical tcgen05 kernel of this build, cfg2 (profiles/): 1.366 PF/s bf16;
+    // FP8: the 256 x 128 block-scaled pair tile
+    p.flops_mul = dtype <= 1 ? 1.366e15 : (dtype == 2 ? 0.66e15 : dtype == 4 ? 2.0e15 : 60e12);
     p.flops_add = 148.0 * 128.0 * 1.3e9;
     p.beta = 6.55e12 / bytes;
     // group_combine_kernel measured ~4.4 TB/s of read+write traffic (cfg2)
@@ -176,7 +178,7 @@ Profile default_profile(int dtype) {
     // profiles/r01f_cfg3_decision.json: Strassen median overhead +8 % for
     // 16-bit data and -4 % for tf32, Laderman / Strassen^2 through alpha)
     p.alpha_partial = 8.0;
-    p.epi_overhead = bytes == 2.0 ? 0.08 : -0.04;
+    p.epi_overhead = bytes <= 2.0 ? 0.08 : -0.04;
     if (const char* env = diag_env("LCMA_PROFILE")) {
         const char* keys[5] = {"flops_mul=", "flops_add=", "beta_elems=", "beta_combine=", "alpha_partial="};
         double* dst[5] = {&p.flops_mul, &p.flops_add, &p.beta, &p.beta_combine, &p.alpha_partial};

@@ -39,7 +39,13 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int64_t roundup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-int elem_bytes(lcma_dtype d) { return (d == LCMA_BF16 || d == LCMA_FP16) ? 2 : 4; }
+// input element bytes (FP8 plans take bf16 A and B and quantize them)
+int elem_bytes(lcma_dtype d) { return (d == LCMA_BF16 || d == LCMA_FP16 || d == LCMA_FP8_E4M3) ? 2 : 4; }
+// FP8 operand bytes of the quantized A~ / B~ (E4M3) and their UE8M0 scale
+// chunks: 4 bytes per operand row and 128-element k-block (512-byte chunks)
+size_t fp8_operand_bytes(int64_t R, int64_t rows, int64_t Kb) {
+    return (size_t)R * rows * Kb + (size_t)R * rows * (Kb / 128) * 4;
+}
 
 int device_sm_count() {
     int dev = 0, sms = 0;
@@ -100,6 +106,7 @@ struct lcma_plan_s {
     int variant;
     int64_t Mb, Nb, Kb;
     int BK, e;
+    int oe = 0;                    // operand element bytes in the GEMM (FP8: 1)
     int nX, nZ, G, nK;
     int ctas, cg, bn, q, tail_c, swz;
     int n_whole, dyn, dyn_tail;
@@ -193,9 +200,17 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
     *out = nullptr;
     const lcma_plan_desc& d = *desc;
     if (d.M < 1 || d.N < 1 || d.K < 1) return fail(LCMA_ERR_INVALID_VALUE, "M, N, K must be >= 1");
-    if (d.dtype < LCMA_BF16 || d.dtype > LCMA_FP32) return fail(LCMA_ERR_INVALID_VALUE, "bad dtype");
+    if (d.dtype < LCMA_BF16 || d.dtype > LCMA_FP8_E4M3) return fail(LCMA_ERR_INVALID_VALUE, "bad dtype");
+    const bool fp8 = d.dtype == LCMA_FP8_E4M3;
     lcma_dtype od = d.out_dtype;
-    if (od != d.dtype && od != LCMA_FP32) return fail(LCMA_ERR_NOT_SUPPORTED, "out_dtype must equal dtype or be FP32");
+    if (fp8) {
+        // C of the FP8 path is bf16 (or fp32); B is N x K (K-major E4M3 operand)
+        if (od == LCMA_FP8_E4M3) od = LCMA_BF16;
+        if (od != LCMA_BF16 && od != LCMA_FP32) return fail(LCMA_ERR_NOT_SUPPORTED, "FP8 output is bf16 or fp32");
+        if (d.b_layout != 1) return fail(LCMA_ERR_NOT_SUPPORTED, "FP8 needs B stored N x K (b_layout 1)");
+    }
+    if (!fp8 && od != d.dtype && od != LCMA_FP32)
+        return fail(LCMA_ERR_NOT_SUPPORTED, "out_dtype must equal dtype or be FP32");
     if (d.dtype == LCMA_TF32 && od != LCMA_FP32 && od != LCMA_TF32)
         return fail(LCMA_ERR_NOT_SUPPORTED, "tf32 output is fp32");
     if (d.b_layout != 0 && d.b_layout != 1) return fail(LCMA_ERR_INVALID_VALUE, "b_layout must be 0 or 1");
@@ -207,7 +222,9 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
 
     auto* p = new lcma_plan_s();
     p->d = d;
+    p->d.out_dtype = od;
     p->e = e;
+    p->oe = fp8 ? 1 : e;
     p->hw = d.hw ? Profile{d.hw->flops_mul, d.hw->flops_add, d.hw->beta_elems}
                  : default_profile((int)d.dtype);
     if (!(p->hw.flops_mul > 0 && p->hw.flops_add > 0 && p->hw.beta > 0)) {
@@ -262,6 +279,13 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             delete p;
             return fail(LCMA_ERR_NOT_SUPPORTED, "fp32 (SIMT) LCMA runs the unfused variant only");
         }
+    } else if (fp8) {
+        // FP8: the quantizing combines + the block-scaled fused-Combine-H GEMM
+        if (variant == LCMA_VARIANT_AUTO) variant = LCMA_VARIANT_FUSED_H;
+        if (variant != LCMA_VARIANT_FUSED_H) {
+            delete p;
+            return fail(LCMA_ERR_NOT_SUPPORTED, "FP8 LCMA runs the fused Combine H variant only");
+        }
     } else {
         // composed schemes run two-level (measured 1.06-1.34x faster than the
         // flat 49-product fused kernel: its 11 live partials per CTA spill L2)
@@ -302,7 +326,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         p->ctas = 0;
         p->cg = 1;
     } else {
-        p->BK = 128 / e;
+        p->BK = 128 / p->oe;
         const int sms = device_sm_count();
         p->ctas = d.num_ctas > 0 ? std::min(d.num_ctas, sms) : sms;
         p->cg = 2;
@@ -318,6 +342,8 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         const int tileM = kBM * p->cg;
         p->bn = kBN;
         if (const char* e_bn = diag_env("LCMA_BN")) p->bn = std::atoi(e_bn) == 128 ? 128 : 256;
+        // FP8: 2 x 128 accumulator columns leave TMEM room for the scale factors
+        if (fp8) { p->bn = 128; p->cg = 2; }
         const int BNp = p->bn;
         if (classical) {
             p->nX = (int)cdiv(d.M, tileM);
@@ -398,7 +424,19 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         p->off_sched = off;                    // dynamic-schedule ticket counter
         off = align256(off + 256);
     }
-    if (!classical) {
+    if (fp8) {
+        // quantized operands (+ scale chunks), per call for classical too
+        if (!classical) {
+            p->off_P = off;
+            off = align256(off + (size_t)3 * p->ctas * mn * kBM * p->bn * sizeof(float));
+            p->off_flags = off;
+            off = align256(off + (size_t)p->ctas * sizeof(int));
+        }
+        p->off_At = off;
+        off = align256(off + fp8_operand_bytes(S.R, p->Mb, p->Kb));
+        p->off_Bt = off;
+        off = align256(off + fp8_operand_bytes(S.R, p->Nb, p->Kb));
+    } else if (!classical) {
         if (d.dtype != LCMA_FP32 && (variant == LCMA_VARIANT_FUSED_H || variant == LCMA_VARIANT_PRODUCER)) {
             p->off_P = off;
             off = align256(off + (size_t)3 * p->ctas * mn * kBM * p->bn * sizeof(float));
@@ -422,7 +460,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         }
     }
     p->ws_bytes = off;
-    p->bt_bytes = classical ? 0 : (size_t)S.R * p->Kb * p->Nb * e;
+    p->bt_bytes = fp8 ? fp8_operand_bytes(S.R, p->Nb, p->Kb) : classical ? 0 : (size_t)S.R * p->Kb * p->Nb * e;
 
     // ---- info
     lcma_plan_info& I = p->info;
@@ -603,15 +641,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-lcma_status make_map(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64_t cols, uint64_t rows,
-                     uint32_t box_c, uint32_t box_r,
-                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+lcma_status make_map_t(CUtensorMap* m, const void* ptr, CUtensorMapDataType t, int e, uint64_t cols,
+                       uint64_t rows, uint32_t box_c, uint32_t box_r,
+                       CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     auto fn = encode_fn();
     if (!fn) return fail(LCMA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    CUtensorMapDataType t = dt == LCMA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                            : dt == LCMA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
-                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    const int e = elem_bytes(dt);
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {cols * (cuuint64_t)e};
     cuuint32_t box[2] = {box_c, box_r};
@@ -626,6 +660,15 @@ lcma_status make_map(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64_t co
         return fail(LCMA_ERR_CUDA, buf);
     }
     return LCMA_OK;
+}
+
+lcma_status make_map(CUtensorMap* m, const void* ptr, lcma_dtype dt, uint64_t cols, uint64_t rows,
+                     uint32_t box_c, uint32_t box_r,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+    const CUtensorMapDataType t = dt == LCMA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                  : dt == LCMA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    return make_map_t(m, ptr, t, elem_bytes(dt), cols, rows, box_c, box_r, swz);
 }
 
 // MN-major B (rows x cols row-major, cols % epr == 0) as a 3-D map
@@ -683,16 +726,16 @@ lcma_status check_launch(const char* what) {
 
 // The dynamic shared-memory limit is a per-device function attribute: set it
 // once per (instantiation, device).
-template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false>
+template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false, bool F8 = false>
 lcma_status ensure_smem_attr() {
     static std::once_flag once[kMaxDev];
     static cudaError_t err[kMaxDev];
     const int dv = current_device();
     if (dv < 0) return fail(LCMA_ERR_CUDA, "no current CUDA device (or ordinal >= 64)");
     std::call_once(once[dv], [dv] {
-        err[dv] = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF, DYN>,
+        err[dv] = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF, DYN, F8>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF>::kSmemBytes);
+                                       Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF, F8>::kSmemBytes);
     });
     if (err[dv] != cudaSuccess)
         return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err[dv]));
@@ -769,6 +812,37 @@ lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, boo
     return check_launch("group_combine_kernel");
 }
 
+// FP8: group combine of one bf16 operand with the 1 x 128 quantization fused
+// in: dst = E4M3 [R][E0][Kb] followed by the UE8M0 scale chunks.
+// A: M x K, blocks (i, l), coef U[r][i][l]; B: N x K, blocks (j, l), coef V[r][l][j].
+lcma_status launch_combine_q8(const lcma_plan_s* p, const void* src, void* dst, bool is_b, cudaStream_t st) {
+    const Scheme& S = p->sch;
+    CombineQ8Params c;
+    std::memset(&c, 0, sizeof(c));
+    c.src = reinterpret_cast<const uint16_t*>(src);
+    c.dst = reinterpret_cast<uint8_t*>(dst);
+    c.R = S.R;
+    if (!is_b) {
+        c.rows = p->d.M; c.cols = p->d.K; c.E0 = p->Mb; c.E1 = p->Kb; c.P = S.m; c.Q = S.k;
+    } else {
+        c.rows = p->d.N; c.cols = p->d.K; c.E0 = p->Nb; c.E1 = p->Kb; c.P = S.n; c.Q = S.k;
+    }
+    c.sf = reinterpret_cast<uint32_t*>(c.dst + (size_t)S.R * c.E0 * c.E1);
+    const int pq = c.P * c.Q;
+    const int inst = pq <= 1 ? 1 : pq <= 4 ? 4 : pq <= 9 ? 9 : 16;
+    if (S.R > kCombMaxR || pq > 16) return fail(LCMA_ERR_NOT_SUPPORTED, "scheme too large for the FP8 combine");
+    for (int r = 0; r < S.R; ++r)
+        for (int a = 0; a < c.P; ++a)
+            for (int b = 0; b < c.Q; ++b)
+                c.coef[r * inst + a * c.Q + b] = !is_b ? S.u(r, a, b) : S.v(r, b, a);
+    const int g = grid_for(c.E0 * (c.E1 / 8), 256);
+    if (inst == 1) group_combine_q8_kernel<1><<<g, 256, 0, st>>>(c);
+    else if (inst == 4) group_combine_q8_kernel<4><<<g, 256, 0, st>>>(c);
+    else if (inst == 9) group_combine_q8_kernel<9><<<g, 256, 0, st>>>(c);
+    else group_combine_q8_kernel<16><<<g, 256, 0, st>>>(c);
+    return check_launch("group_combine_q8_kernel");
+}
+
 // Combine H (Eq. 6) of scheme S over H [R][Mb][Nb] fp32 into C (M x N, crop).
 lcma_status launch_combine_h_ex(const lcma_plan_s* p, const Scheme& S, long long Mb, long long Nb, const float* H,
                                 void* C, cudaStream_t st) {
@@ -814,11 +888,14 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     // REGH: the instantiation with a register partial home (fused Combine H of
     // an LCMA scheme on 256-column pair tiles); classical / unfused GEMMs use
     // the one without (no 128 live registers reserved in the epilogue)
-    const bool regh = !classical && !H && p->cg == 2 && p->bn == 256;
+    const bool f8 = p->d.dtype == LCMA_FP8_E4M3;
+    const bool regh = f8 ? (!classical && !H) : (!classical && !H && p->cg == 2 && p->bn == 256);
     // the plan only sets dyn / dyn_tail for 256-column pair kernels
     const bool dyn = (p->dyn || p->dyn_tail) && sched && !pf;
-    if (pf || dyn) qf = 0;
-    lcma_status rs = pf == 2 ? ensure_smem_attr<2, 256, 0, true, 2>()
+    if (pf || dyn || f8) qf = 0;
+    lcma_status rs = f8 ? (regh ? ensure_smem_attr<2, 128, 0, true, 0, false, true>()
+                                : ensure_smem_attr<2, 128, 0, false, 0, false, true>())
+                   : pf == 2 ? ensure_smem_attr<2, 256, 0, true, 2>()
                    : pf == 1 ? ensure_smem_attr<2, 256, 0, true, 1>()
                    : p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
                                                 : (qf ? ensure_smem_attr<2, 256, 1, true>()
@@ -831,13 +908,22 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     const lcma_dtype dt = p->d.dtype;
     const int epr = 128 / p->e;           // elements per 128-byte row
     CUtensorMap ta, tb;
+    const bool b_mn = p->d.b_layout == 0;
+    bool b3d = false;
+    if (f8) {
+        // quantized operands: A~ [R][Mb][Kb], B~ [R][Nb][Kb] E4M3 (K-major, 128
+        // elements per 128-byte row), each followed by its scale chunks
+        rs = make_map_t(&ta, Aop, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p->Kb, (uint64_t)S.R * p->Mb, 128, kBM);
+        if (rs != LCMA_OK) return rs;
+        rs = make_map_t(&tb, Bop, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p->Kb, (uint64_t)S.R * p->Nb, 128,
+                        p->bn / p->cg);
+        if (rs != LCMA_OK) return rs;
+    } else {
     // A operand: K-major rows (PF: the raw A, its blocks are combined in the kernel)
     const uint64_t a_cols = (classical || pf) ? p->d.K : p->Kb;
     const uint64_t a_rows = (classical || pf) ? p->d.M : (uint64_t)S.R * p->Mb * p->nbatch;
     rs = make_map(&ta, Aop, dt, a_cols, a_rows, epr, kBM);
     if (rs != LCMA_OK) return rs;
-    const bool b_mn = p->d.b_layout == 0;
-    bool b3d = false;
     if (!b_mn) {   // N x K (K-major); PF 2: the raw B, its blocks are combined in the kernel
         const uint64_t cols = (classical || pf == 2) ? p->d.K : p->Kb;
         const uint64_t rows = (classical || pf == 2) ? p->d.N : (uint64_t)S.R * p->Nb * p->nbatch;
@@ -856,6 +942,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         if (!b3d) rs = make_map(&tb, Bop, dt, cols, rows, epr, p->BK, swz);
     }
     if (rs != LCMA_OK) return rs;
+    }
 
     GemmParams g;
     std::memset(&g, 0, sizeof(g));
@@ -872,8 +959,25 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     if (const char* v = diag_env("LCMA_TF32_MN_LT")) g.b_layout_type = std::atoi(v);
     if (const char* v = diag_env("LCMA_TF32_MN_SBO")) g.b_sbo = std::atoi(v);
     g.tf32 = dt == LCMA_TF32;
-    g.idesc = ptx::make_idesc(dt == LCMA_BF16 ? 1u : dt == LCMA_FP16 ? 0u : 2u, kBM * p->cg, p->bn,
-                              b_mn ? 1u : 0u, 0u);
+    g.idesc = f8 ? ptx::make_idesc_mxf8(kBM * p->cg, p->bn)
+                 : ptx::make_idesc(dt == LCMA_BF16 ? 1u : dt == LCMA_FP16 ? 0u : 2u, kBM * p->cg, p->bn,
+                                   b_mn ? 1u : 0u, 0u);
+    if (f8) {
+        // UE8M0 scale chunks behind the operands, as [2 * chunks][256] byte maps
+        g.a_rows_per_r = (int)p->Mb;
+        g.b_rows_per_r = (int)p->Nb;
+        g.sf_nkb = (int)(p->Kb / 128);
+        const uint64_t ca = (uint64_t)S.R * (p->Mb / 128) * (p->Kb / 128);
+        const uint64_t cb = (uint64_t)S.R * (p->Nb / 128) * (p->Kb / 128);
+        const uint8_t* sa = reinterpret_cast<const uint8_t*>(Aop) + (size_t)S.R * p->Mb * p->Kb;
+        const uint8_t* sb = reinterpret_cast<const uint8_t*>(Bop) + (size_t)S.R * p->Nb * p->Kb;
+        rs = make_map_t(&g.sfa_map, sa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 256, 2 * ca, 256, 2,
+                        CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (rs != LCMA_OK) return rs;
+        rs = make_map_t(&g.sfb_map, sb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 256, 2 * cb, 256, 2,
+                        CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (rs != LCMA_OK) return rs;
+    }
     g.W = p->ctas / p->cg; g.q = p->q; g.tail_c = p->tail_c; g.swz = p->swz;
     g.n_whole = p->n_whole;
     g.dyn = dyn && p->dyn ? 1 : 0;
@@ -990,7 +1094,12 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     cfg.attrs = attr;
     cfg.numAttrs = na;
     cudaError_t e;
-    if (pf) {
+    if (f8) {
+        using CF = Cfg<2, 128, 0, false, 0, true>;
+        cfg.dynamicSmemBytes = CF::kSmemBytes;
+        e = regh ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 128, 0, true, 0, false, true>, ta, tb, g)
+                 : cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 128, 0, false, 0, false, true>, ta, tb, g);
+    } else if (pf) {
         g.kgrid = S.k;
         g.pf_Kb = (int)p->Kb;
         for (int r = 0; r < S.R; ++r) {
@@ -1098,6 +1207,23 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
     uint8_t* w = reinterpret_cast<uint8_t*>(ws);
     const bool classical = p->scheme_id == SCHEME_CLASSICAL;
     const bool fp32 = p->d.dtype == LCMA_FP32;
+    if (p->d.dtype == LCMA_FP8_E4M3) {
+        // Combine A with the 1 x 128 quantization fused in, the same
+        // for B unless B~ was quantized offline, then the block-scaled
+        // GEMM with the fused Combine H (classical: quantization passes + GEMM)
+        void* At = w + p->off_At;
+        lcma_status rq = launch_combine_q8(p, A, At, false, st);
+        if (rq != LCMA_OK) return rq;
+        const void* Bq = Bt_user;
+        if (!Bq) {
+            rq = launch_combine_q8(p, B, w + p->off_Bt, true, st);
+            if (rq != LCMA_OK) return rq;
+            Bq = w + p->off_Bt;
+        }
+        return launch_umma(p, At, Bq, C, classical ? nullptr : reinterpret_cast<float*>(w + p->off_P),
+                           classical ? nullptr : reinterpret_cast<int*>(w + p->off_flags),
+                           reinterpret_cast<int*>(w + p->off_sched), nullptr, st);
+    }
     if (classical) {
         if (fp32) {
             if (p->d.out_dtype != LCMA_FP32) return fail(LCMA_ERR_NOT_SUPPORTED, "fp32 output only");
@@ -1190,7 +1316,8 @@ extern "C" lcma_status lcma_gemm(lcma_plan_t p, const void* A, const void* B, vo
 extern "C" lcma_status lcma_gemm_precombined(lcma_plan_t p, const void* A, const void* Bt, void* C,
                                              void* ws, size_t ws_bytes, void* stream) {
     if (!p || !Bt) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
-    if (p->scheme_id == SCHEME_CLASSICAL) return run(p, A, Bt, nullptr, C, ws, ws_bytes, stream);
+    if (p->scheme_id == SCHEME_CLASSICAL && p->d.dtype != LCMA_FP8_E4M3)
+        return run(p, A, Bt, nullptr, C, ws, ws_bytes, stream);   // classical: Bt is B itself
     return run(p, A, nullptr, Bt, C, ws, ws_bytes, stream);
 }
 
@@ -1200,8 +1327,21 @@ extern "C" lcma_status lcma_precombine_b(lcma_plan_t p, const void* B, void* Bt,
     if (!p || !B || !Bt) return fail(LCMA_ERR_INVALID_VALUE, "null argument");
     if ((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(Bt)) & 15)
         return fail(LCMA_ERR_MISALIGNED, "device pointers must be 16-byte aligned");
+    if (p->d.dtype == LCMA_FP8_E4M3)      // quantized B~ (classical: B itself, quantized)
+        return launch_combine_q8(p, B, Bt, true, reinterpret_cast<cudaStream_t>(stream));
     if (p->scheme_id == SCHEME_CLASSICAL) return fail(LCMA_ERR_INVALID_VALUE, "classical plan has no Bt");
     return launch_combine(p, B, Bt, true, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Workspace layout accessor: byte offset of region `which` (0: A~ -- for
+// LCMA_FP8_E4M3 the E4M3 A~ followed by its scale chunks --, 1: B~ when B is
+// combined per call) inside the plan's workspace.
+extern "C" lcma_status lcma_workspace_region(lcma_plan_t p, int32_t which, size_t* offset) {
+    if (!p || !offset || which < 0 || which > 1) return fail(LCMA_ERR_INVALID_VALUE, "bad argument");
+    const bool has = p->d.dtype == LCMA_FP8_E4M3 || p->scheme_id != SCHEME_CLASSICAL;
+    if (!has) return fail(LCMA_ERR_INVALID_VALUE, "plan has no A~ / B~ region");
+    *offset = which == 0 ? p->off_At : p->off_Bt;
+    return LCMA_OK;
 }
 
 // Measurement hook: when set (non-NULL cudaEvent_t handles), every following

@@ -331,6 +331,49 @@ __device__ __forceinline__ void mma_tf32_ss_cg2(uint32_t d_tmem, uint64_t a_desc
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// FP8 E4M3 x E4M3 with per-32-K UE8M0 block scales read from TMEM
+// (kind::mxf8f6f4.block_scale, scale_vec::1X): D (+)= (A * sfa) (B * sfb)
+template <int CG>
+__device__ __forceinline__ void mma_mxf8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+    if constexpr (CG == 1)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %6, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale.scale_vec::1X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
+                d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(sfa_tmem), "r"(sfb_tmem), "r"(accumulate)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %6, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale.scale_vec::1X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
+                d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(sfa_tmem), "r"(sfb_tmem), "r"(accumulate)
+            : "memory");
+}
+// shared memory -> TMEM: 32 rows x 128 bits, broadcast to the four 32-lane
+// quarters (the block-scale factor layout); in pair mode each CTA's own
+// shared memory goes to its own TMEM.  Ordered with later tcgen05.mma.
+template <int CG>
+__device__ __forceinline__ void tmem_cp_32x128b_x4(uint32_t taddr, uint64_t s_desc) {
+    if constexpr (CG == 1)
+        asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(s_desc) : "memory");
+    else
+        asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(s_desc) : "memory");
+}
+// Instruction descriptor, kind::mxf8f6f4.block_scale with E4M3 A and B,
+// UE8M0 scales, fp32 accumulation:
+//   [4,6) B scale-factor id  [7,10) a_format (E4M3 = 0)  [10,13) b_format
+//   [15] A major (0 = K)  [16] B major  [17,23) N >> 3  [23] scale format
+//   (1 = E8M0)  [24,29) M >> 4  [29,31) A scale-factor id
+__host__ __device__ constexpr uint32_t make_idesc_mxf8(uint32_t M, uint32_t N) {
+    return ((N >> 3) << 17) | (1u << 23) | ((M >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t idesc_sf_ids(uint32_t idesc, uint32_t a_id, uint32_t b_id) {
+    return idesc | (b_id << 4) | (a_id << 29);
+}
 // 2-SM commit: arrive on the barrier at the same smem offset in every CTA of
 // `mask` once the pair's MMAs issued so far have completed.
 __device__ __forceinline__ void mma_commit_cg2_mc(uint64_t* bar, uint16_t mask) {

@@ -72,14 +72,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // PF: producer-fused combines (variant 3): 1 = Combine A, 2 = Combine A and B;
 // a staging slot per stage for the second source block of each, and
 // second A source block, no shared-memory partial area.
-template <int CG, int BN = kBN, int QF = 0, bool NP = false, int PF = 0>
+// F8: FP8 E4M3 operands (128 elements per 128-byte row) plus, per stage, the
+// 512-byte UE8M0 scale chunks of the A rows and of the B columns (1 x 128
+// block scaling, reading 23).
+template <int CG, int BN = kBN, int QF = 0, bool NP = false, int PF = 0, bool F8 = false>
 struct Cfg {
     static constexpr int kTileM = kBM * CG;                  // rows per group tile
     static constexpr int kBNc = BN / CG;                     // B columns staged per CTA
     static constexpr int kABytes = kBM * 128;                // 128 rows x 128 bytes
     static constexpr int kBBytes = kBNc * 128;               // kBNc x 128 B (K-major) or chunks (MN-major)
+    static constexpr int kSfBytes = F8 ? 1024 : 0;              // scale chunks: A rows, B columns
     static constexpr int kStageBytes =
-        kABytes + kBBytes + (PF ? kABytes : 0) + (PF == 2 ? kBBytes : 0);   // PF: + staging
+        kABytes + kBBytes + (PF ? kABytes : 0) + (PF == 2 ? kBBytes : 0) + kSfBytes;   // PF: + staging
     // one C_ij partial kept in shared memory (fused Combine H, whole groups):
     // 128 rows x BN (QF) or BN/2 (column half 0) fp32
     static constexpr int kPartialSmem = (NP || PF) ? 0 : kBM * (QF ? BN : BN / 2) * 4;
@@ -106,6 +110,12 @@ enum UnitRole : int { ROLE_WHOLE = 0, ROLE_OWNER = 1, ROLE_CONTRIB = 2 };
 enum PartialHome : int { HOME_REG = -1, HOME_SMEM = -2 };
 
 struct GemmParams {
+    // F8: the UE8M0 scale chunks of A~ and B~ as 2-D byte maps [2 * chunks][256]
+    // (one 512-byte chunk per 128 rows x 128 K of an operand); chunk index =
+    // (operand row / 128) * sf_nkb + k-block
+    alignas(64) CUtensorMap sfa_map;
+    alignas(64) CUtensorMap sfb_map;
+    int sf_nkb;            // k-blocks per operand row (Kb / 128)
     // problem / blocking
     int nX, nZ;            // group tiles along M, N: Mb/kTileM, Nb/kBN
     int G;                 // groups = nX * nZ
@@ -618,12 +628,13 @@ __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, unsig
 }
 
 // ------------------------------------------------------------ the kernel
-template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false>
+template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false, bool F8 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ GemmParams p) {
-    using C_ = Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF>;
+    using C_ = Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF, F8>;
+    static_assert(!F8 || (BN == 128 && PF == 0), "FP8: 128-column tiles (2 x 128 accumulator columns + scales in TMEM)");
     constexpr int kStages = C_::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -739,6 +750,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     ptx::tma_load_2d(sb + c * b_bytes_chunk, &tmap_b, &full_bar[stage],
                                                      b_col0 + c * p.BK, r * p.b_rows_per_r + kcol);
                             }
+                            if constexpr (F8) {
+                                const int ca = ((r * p.a_rows_per_r + x * C_::kTileM) >> 7) * p.sf_nkb + kb;
+                                const int cb = ((r * p.b_rows_per_r + z * BN) >> 7) * p.sf_nkb + kb;
+                                ptx::tma_load_2d(sb + C_::kBBytes, &p.sfa_map, &full_bar[stage], 0, 2 * ca);
+                                ptx::tma_load_2d(sb + C_::kBBytes + 512, &p.sfb_map, &full_bar[stage], 0, 2 * cb);
+                            }
                         } else {
                             // only the leader arms its barrier (with both CTAs' bytes);
                             // the peer's TMA completes bytes on the leader's barrier
@@ -799,6 +816,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                      (c1 / p.ngrid) * p.pf_Kb + kcol, (c1 % p.ngrid) * p.pf_Nb + b_col0);
                             } else if (!p.b_mn_major) {
                                 ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol_b);
+                                if constexpr (F8) {
+                                    // scale chunks: this CTA's 128 A rows; the pair tile's B columns
+                                    // (both CTAs hold the same chunk: the MMA of each CTA scales
+                                    // all BN columns of its accumulator rows)
+                                    const int ca = (a_row >> 7) * p.sf_nkb + kb;
+                                    const int cb = ((r * p.b_rows_per_r + z * BN) >> 7) * p.sf_nkb + kb;
+                                    ptx::tma_load_2d_cg2(sb + C_::kBBytes, &p.sfa_map, lbar, 0, 2 * ca);
+                                    ptx::tma_load_2d_cg2(sb + C_::kBBytes + 512, &p.sfb_map, lbar, 0, 2 * cb);
+                                }
                             } else if (p.b_3d) {
                                 ptx::tma_load_3d_cg2(sb, &tmap_b, lbar, 0, r * p.b_rows_per_r + kcol,
                                                      b_col0 / p.BK);
@@ -870,7 +896,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t ad = a_desc0 + (uint64_t)(stage * kStageStep);
                         const uint64_t bd = b_desc0 + (uint64_t)(stage * kStageStep);
                         if (ptx::elect_one()) {
-                            if (tf32) {
+                            if constexpr (F8) {
+                                // scales of this stage -> TMEM (columns 2*BN + 8*stage: A rows,
+                                // + 4: B columns), then the four K = 32 block-scaled MMAs; the
+                                // copy and the MMAs execute in issue order
+                                const uint32_t sf_t = tmem_base + 2 * BN + 8 * stage;
+                                const uint32_t sf_s = smem0 + stage * C_::kStageBytes + C_::kABytes + C_::kBBytes;
+                                ptx::tmem_cp_32x128b_x4<CG>(sf_t, ptx::smem_desc(sf_s, 0, 128, 0));
+                                ptx::tmem_cp_32x128b_x4<CG>(sf_t + 4, ptx::smem_desc(sf_s + 512, 0, 128, 0));
+#pragma unroll
+                                for (int ks = 0; ks < 4; ++ks) {
+                                    const uint32_t accum = (kb | ks) ? 1u : 0u;
+                                    ptx::mma_mxf8_ss<CG>(d_tmem, ad + 2 * ks, bd + b_step * ks,
+                                                         ptx::idesc_sf_ids(idesc, ks, ks), sf_t, sf_t + 4, accum);
+                                }
+                            } else if (tf32) {
 #pragma unroll
                                 for (int ks = 0; ks < 4; ++ks) {
                                     const uint32_t accum = (kb | ks) ? 1u : 0u;

@@ -13,7 +13,8 @@ from __future__ import annotations
 
 import torch
 
-_TORCH_DT = {0: torch.bfloat16, 1: torch.float16, 2: torch.float32, 3: torch.float32}
+_TORCH_DT = {0: torch.bfloat16, 1: torch.float16, 2: torch.float32, 3: torch.float32,
+             4: torch.bfloat16}   # 4 = FP8 path: bf16 inputs
 
 
 def seed_for(cfg: int, idx: int, which: str) -> int:
@@ -27,6 +28,12 @@ def matrix(rows: int, cols: int, dtype_code: int, seed: int, dist: str = "unifor
     g.manual_seed(seed)
     if dist == "uniform":
         x = torch.rand((rows, cols), generator=g, dtype=torch.float32) * 2.0 - 1.0
+    elif dist == "uniform_coarse":
+        # U[-1,1) with |x| < 2^-8 set to 0: after the bf16 cast every value
+        # has an exponent in [-8, -1], so fp32 sums of a few of them are exact
+        # (the FP8 tests compare quantized bytes bit for bit)
+        x = torch.rand((rows, cols), generator=g, dtype=torch.float32) * 2.0 - 1.0
+        x = torch.where(x.abs() < 2.0 ** -8, torch.zeros_like(x), x)
     elif dist == "positive":
         x = torch.rand((rows, cols), generator=g, dtype=torch.float32)
     elif dist == "int":
