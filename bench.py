@@ -255,6 +255,39 @@ def _tf32_corner(L, inputs, torch):
     return out
 
 
+def _fp8_lines(L, inputs, torch):
+    """FP8 E4M3 with 1 x 128 block scaling, quantization fused into
+    Combine A: classical (A quantized per call, B offline) vs
+    Strassen (Combine A + quantize per call, B~ quantized offline) and both
+    with B per call, at cfg2 and cfg5 and, for the paper's small-M claim
+    (P:471), at M = 1024 / 2048 of the cfg2 weight.  Interleaved timing."""
+    out = {"dtype": "e4m3 (bf16 in / bf16 out, 1x128 UE8M0 scales, fp32 accumulation)",
+           "timing": "median of interleaved rounds"}
+    for tag, (M, N, K), rounds in (("cfg2", (8192, 14336, 4096), 5), ("cfg5", (32768, 28672, 8192), 3),
+                                   ("m1024", (1024, 14336, 4096), 5), ("m2048", (2048, 14336, 4096), 5)):
+        A, B = inputs.operands(M, N, K, L.FP8, 601, 602, b_layout=1)
+        A, B = A.cuda(), B.cuda()
+        fns, keep = {}, []
+        for algo in ("classical", "strassen"):
+            p = L.Plan(M, N, K, dtype=L.FP8, algo=algo, b_layout=1)
+            C, ws = p.empty_c(), p.workspace()
+            Bt = p.precombine_b(B)
+            fns[algo] = (lambda p=p, C=C, ws=ws: p.gemm(A, B, C, ws))
+            fns[algo + "_static_b"] = (lambda p=p, C=C, ws=ws, Bt=Bt: p.gemm_precombined(A, Bt, C, ws))
+            keep += [p, C, ws, Bt]
+        med = _interleaved(fns, 2 if M * N * K > 1e12 else 5, rounds=rounds)
+        fl = 2.0 * M * N * K
+        r = {"shape": [M, N, K]}
+        for n, ms in med.items():
+            r[n + "_tflops"] = fl / (ms * 1e-3) / 1e12
+        r["strassen_vs_classical"] = med["classical"] / med["strassen"]
+        r["strassen_static_b_vs_classical_static_b"] = med["classical_static_b"] / med["strassen_static_b"]
+        out[tag] = r
+        del fns, keep, A, B
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -359,6 +392,7 @@ def run_ours(args):
         if not args.no_large:
             ref["large_llama_ffn"] = _large_shape(L, inputs, torch, args)
             ref["cfg3_tf32_corner"] = _tf32_corner(L, inputs, torch)
+            ref["fp8"] = _fp8_lines(L, inputs, torch)
         torch.cuda.empty_cache()
 
     # ---- end to end through the public API with HOST buffers: every step

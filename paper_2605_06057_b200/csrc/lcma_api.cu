@@ -735,7 +735,7 @@ lcma_status ensure_smem_attr() {
     std::call_once(once[dv], [dv] {
         err[dv] = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF, DYN, F8>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF, F8>::kSmemBytes);
+                                       KernelCfg<CG, BN, QF, REGH, PF, F8>::kSmemBytes);
     });
     if (err[dv] != cudaSuccess)
         return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err[dv]));
@@ -835,7 +835,10 @@ lcma_status launch_combine_q8(const lcma_plan_s* p, const void* src, void* dst, 
         for (int a = 0; a < c.P; ++a)
             for (int b = 0; b < c.Q; ++b)
                 c.coef[r * inst + a * c.Q + b] = !is_b ? S.u(r, a, b) : S.v(r, b, a);
-    const int g = grid_for(c.E0 * (c.E1 / 8), 256);
+    // one 8-element vector per thread (no grid-stride cap): the per-product
+    // amax shuffles are latency, more resident warps hide it
+    const long long nb = (c.E0 * (c.E1 / 8) + 255) / 256;
+    const int g = (int)std::min<long long>(nb, 1 << 30);
     if (inst == 1) group_combine_q8_kernel<1><<<g, 256, 0, st>>>(c);
     else if (inst == 4) group_combine_q8_kernel<4><<<g, 256, 0, st>>>(c);
     else if (inst == 9) group_combine_q8_kernel<9><<<g, 256, 0, st>>>(c);
@@ -1095,8 +1098,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     cfg.numAttrs = na;
     cudaError_t e;
     if (f8) {
-        using CF = Cfg<2, 128, 0, false, 0, true>;
-        cfg.dynamicSmemBytes = CF::kSmemBytes;
+        cfg.dynamicSmemBytes = regh ? KernelCfg<2, 128, 0, true, 0, true>::kSmemBytes
+                                    : KernelCfg<2, 128, 0, false, 0, true>::kSmemBytes;
         e = regh ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 128, 0, true, 0, false, true>, ta, tb, g)
                  : cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 128, 0, false, 0, false, true>, ta, tb, g);
     } else if (pf) {

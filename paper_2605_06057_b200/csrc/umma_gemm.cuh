@@ -87,7 +87,9 @@ struct Cfg {
     // one C_ij partial kept in shared memory (fused Combine H, whole groups):
     // 128 rows x BN (QF) or BN/2 (column half 0) fp32
     static constexpr int kPartialSmem = (NP || PF) ? 0 : kBM * (QF ? BN : BN / 2) * 4;
-    static constexpr int kMaxStages = NP ? LCMA_MAX_STAGES_NP : LCMA_MAX_STAGES;
+    // F8: a 128-deep E4M3 k-block is half the MMA time of a 64-deep 16-bit one,
+    // so the ring needs more stages to cover the same load latency
+    static constexpr int kMaxStages = F8 ? 8 : (NP ? LCMA_MAX_STAGES_NP : LCMA_MAX_STAGES);
     // as many stages as fit in 227 KB (minus the partial, alignment slack and
     // barriers), <= LCMA_MAX_STAGES
     static constexpr int kFree = 232448 - 1024 - kBarBytes - kPartialSmem;
@@ -97,10 +99,14 @@ struct Cfg {
 
 // The 256-column pair kernel without a register home is only launched for
 // classical / unfused GEMMs (no partial homes): no shared-memory partial area.
-template <int CG, int BN, int QF, bool REGH>
+// Same for the FP8 instantiation without a register home (classical FP8).
+template <int CG, int BN, int QF, bool REGH, bool F8 = false>
 struct KernelNP {
-    static constexpr bool value = CG == 2 && BN == 256 && QF == 0 && !REGH;
+    static constexpr bool value = CG == 2 && (BN == 256 || F8) && QF == 0 && !REGH;
 };
+// the shared-memory configuration of umma_gemm_kernel<CG, BN, QF, REGH, PF, DYN, F8>
+template <int CG, int BN, int QF, bool REGH, int PF, bool F8>
+using KernelCfg = Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH, F8>::value, PF, F8>;
 
 enum EpiMode : int { EPI_FUSED = 0, EPI_STORE_H = 1 };
 enum OutType : int { OUT_BF16 = 0, OUT_FP16 = 1, OUT_FP32 = 2 };
@@ -633,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ GemmParams p) {
-    using C_ = Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH>::value, PF, F8>;
+    using C_ = KernelCfg<CG, BN, QF, REGH, PF, F8>;
     static_assert(!F8 || (BN == 128 && PF == 0), "FP8: 128-column tiles (2 x 128 accumulator columns + scales in TMEM)");
     constexpr int kStages = C_::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -732,6 +738,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int r = product_at(p, u, t) + qb * p.R;
                     const int a_row = r * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
                     const int b_col0 = z * BN + (int)rank * C_::kBNc;
+                    if constexpr (CG == 2 && PF == 0) {
+#ifdef LCMA_DIAG
+                        // diagnostics build: the general loop below whenever a knob
+                        // changes what the producer issues
+                        const bool lean = !(p.debug & (16 | 32 | 64 | 4096)) && !p.stats && !p.operand_hint;
+#else
+                        constexpr bool lean = true;
+#endif
+                        if (lean && !p.b_mn_major) {
+                            // lean issue loop (K-major A and B, the product build): per
+                            // stage one wait, one expect_tx and the TMA issues with
+                            // every per-product term hoisted -- at 128-deep E4M3
+                            // k-blocks the stage lasts ~270 cycles, so the producer's
+                            // instruction latency, not L2, would otherwise set the pace
+                            const uint32_t lbar0 = ptx::mapa_shared(ptx::smem_u32(&full_bar[0]), 0);
+                            const int b_row = r * p.b_rows_per_r + b_col0;
+                            const int nk = p.nK;
+                            [[maybe_unused]] const int ca0 = (a_row >> 7) * p.sf_nkb;
+                            [[maybe_unused]] const int cb0 = ((r * p.b_rows_per_r + z * BN) >> 7) * p.sf_nkb;
+                            for (int kb = 0; kb < nk; ++kb) {
+                                ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+                                uint8_t* sa = smem + stage * C_::kStageBytes;
+                                const uint32_t lbar = lbar0 + 8u * (uint32_t)stage;
+                                if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kStageBytes * CG);
+                                const int kcol = kb * (F8 ? 128 : p.BK);
+                                ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row);
+                                ptx::tma_load_2d_cg2(sa + C_::kABytes, &tmap_b, lbar, kcol, b_row);
+                                if constexpr (F8) {
+                                    ptx::tma_load_2d_cg2(sa + C_::kABytes + C_::kBBytes, &p.sfa_map, lbar, 0,
+                                                         2 * (ca0 + kb));
+                                    ptx::tma_load_2d_cg2(sa + C_::kABytes + C_::kBBytes + 512, &p.sfb_map, lbar, 0,
+                                                         2 * (cb0 + kb));
+                                }
+                                if (++stage == kStages) { stage = 0; phase ^= 1; }
+                                if constexpr (DYN) {
+                                    if (kb == 0 && t == u.r0) it.advance();
+                                }
+                            }
+                            continue;
+                        }
+                    }
                     for (int kb = 0; kb < p.nK; ++kb) {
                         timed_wait(&empty_bar[stage], phase ^ 1, st_empty);
                         uint8_t* sa = smem + stage * C_::kStageBytes;
@@ -773,12 +820,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // diagnostics (debug bit 6): A tile loaded only on even k-blocks,
                             // i.e. the L2 operand traffic of an A-multicast cluster of 2 pairs
                             const bool skip_a = (p.debug & 64) && (kb & 1);
+                            // diagnostics (debug bit 12, F8): no scale-chunk loads (stale scales)
+                            const bool skip_sf = F8 && (p.debug & 4096);
                             if (leader) {
                                 if constexpr (PF == 2) ptx::mbar_arrive(&full_bar[stage]);   // all bytes on ld_bar
                                 else if constexpr (PF == 1) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kBBytes * CG);
                                 else
                                     ptx::mbar_arrive_expect_tx(&full_bar[stage],
-                                                               (C_::kStageBytes - (skip_a ? C_::kABytes : 0) +
+                                                               (C_::kStageBytes - (skip_a ? C_::kABytes : 0) -
+                                                                (skip_sf ? C_::kSfBytes : 0) +
                                                                 ea * C_::kABytes + eb * C_::kBBytes) * CG);
                             }
                             for (int e = 1; e <= ea; ++e)
@@ -816,7 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                      (c1 / p.ngrid) * p.pf_Kb + kcol, (c1 % p.ngrid) * p.pf_Nb + b_col0);
                             } else if (!p.b_mn_major) {
                                 ptx::tma_load_2d_cg2(sb, &tmap_b, lbar, kcol, r * p.b_rows_per_r + b_col0, ohint, opol_b);
-                                if constexpr (F8) {
+                                if (F8 && !skip_sf) {
                                     // scale chunks: this CTA's 128 A rows; the pair tile's B columns
                                     // (both CTAs hold the same chunk: the MMA of each CTA scales
                                     // all BN columns of its accumulator rows)
@@ -902,8 +952,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 // copy and the MMAs execute in issue order
                                 const uint32_t sf_t = tmem_base + 2 * BN + 8 * stage;
                                 const uint32_t sf_s = smem0 + stage * C_::kStageBytes + C_::kABytes + C_::kBBytes;
-                                ptx::tmem_cp_32x128b_x4<CG>(sf_t, ptx::smem_desc(sf_s, 0, 128, 0));
-                                ptx::tmem_cp_32x128b_x4<CG>(sf_t + 4, ptx::smem_desc(sf_s + 512, 0, 128, 0));
+                                if (!(p.debug & 8192)) {     // diagnostics (bit 13): stale TMEM scales
+                                    ptx::tmem_cp_32x128b_x4<CG>(sf_t, ptx::smem_desc(sf_s, 0, 128, 0));
+                                    ptx::tmem_cp_32x128b_x4<CG>(sf_t + 4, ptx::smem_desc(sf_s + 512, 0, 128, 0));
+                                }
 #pragma unroll
                                 for (int ks = 0; ks < 4; ++ks) {
                                     const uint32_t accum = (kb | ks) ? 1u : 0u;
