@@ -58,6 +58,9 @@ int device_sm_count() {
 }
 
 constexpr int kMaxDev = 64;
+// register-home fused kernel: products of at most this many k-blocks take the
+// C-staging (TMA store) instantiation
+constexpr int kCstMaxNK = 48;
 int current_device() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return -1; }
@@ -430,7 +433,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             p->off_P = off;
             off = align256(off + (size_t)3 * p->ctas * mn * kBM * p->bn * sizeof(float));
             p->off_flags = off;
-            off = align256(off + (size_t)p->ctas * sizeof(int));
+            off = align256(off + (size_t)2 * p->ctas * sizeof(int));   // split flags: contributor + owner units
         }
         p->off_At = off;
         off = align256(off + fp8_operand_bytes(S.R, p->Mb, p->Kb));
@@ -441,7 +444,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             p->off_P = off;
             off = align256(off + (size_t)3 * p->ctas * mn * kBM * p->bn * sizeof(float));
             p->off_flags = off;
-            off = align256(off + (size_t)p->ctas * sizeof(int));
+            off = align256(off + (size_t)2 * p->ctas * sizeof(int));   // split flags: contributor + owner units
         }
         p->off_At = off;
         off = align256(off + (size_t)S.R * p->Mb * p->Kb * e);
@@ -726,16 +729,17 @@ lcma_status check_launch(const char* what) {
 
 // The dynamic shared-memory limit is a per-device function attribute: set it
 // once per (instantiation, device).
-template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false, bool F8 = false>
+template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false, bool F8 = false,
+          bool CST = true>
 lcma_status ensure_smem_attr() {
     static std::once_flag once[kMaxDev];
     static cudaError_t err[kMaxDev];
     const int dv = current_device();
     if (dv < 0) return fail(LCMA_ERR_CUDA, "no current CUDA device (or ordinal >= 64)");
     std::call_once(once[dv], [dv] {
-        err[dv] = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF, DYN, F8>,
+        err[dv] = cudaFuncSetAttribute(umma_gemm_kernel<CG, BN, QF, REGH, PF, DYN, F8, CST>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       KernelCfg<CG, BN, QF, REGH, PF, F8>::kSmemBytes);
+                                       KernelCfg<CG, BN, QF, REGH, PF, F8, CST>::kSmemBytes);
     });
     if (err[dv] != cudaSuccess)
         return fail(LCMA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err[dv]));
@@ -892,6 +896,11 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     // an LCMA scheme on 256-column pair tiles); classical / unfused GEMMs use
     // the one without (no 128 live registers reserved in the epilogue)
     const bool f8 = p->d.dtype == LCMA_FP8_E4M3;
+    // register-home kernel: C through shared memory + TMA stores (one operand
+    // stage fewer) when a product is short (the fused epilogue then paces the
+    // MMA); long products keep 5 stages and store C from registers
+    bool cst_regh = p->nK <= kCstMaxNK;
+    if (const char* v = diag_env("LCMA_CST")) cst_regh = std::atoi(v) != 0;
     const bool regh = f8 ? (!classical && !H) : (!classical && !H && p->cg == 2 && p->bn == 256);
     // the plan only sets dyn / dyn_tail for 256-column pair kernels
     const bool dyn = (p->dyn || p->dyn_tail) && sched && !pf;
@@ -903,7 +912,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
                    : p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
                                                 : (qf ? ensure_smem_attr<2, 256, 1, true>()
                                                       : regh ? (dyn ? ensure_smem_attr<2, 256, 0, true, 0, true>()
-                                                                    : ensure_smem_attr<2, 256, 0, true>())
+                                                                    : cst_regh ? ensure_smem_attr<2, 256, 0, true>()
+                                                                    : ensure_smem_attr<2, 256, 0, true, 0, false, false, false>())
                                                              : (dyn ? ensure_smem_attr<2, 256, 0, false, 0, true>()
                                                                     : ensure_smem_attr<2, 256>())))
                                 : (p->bn == 128 ? ensure_smem_attr<1, 128>() : ensure_smem_attr<1, 256>());
@@ -999,6 +1009,20 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         g.c_v8 = ((reinterpret_cast<uintptr_t>(C) & 31) == 0 && (g.ldc * ce) % 32 == 0) ? 1 : 0;
         if (diag_env("LCMA_NO_V8")) g.c_v8 = 0;
         g.c_cs = diag_env("LCMA_C_CS") ? std::atoi(diag_env("LCMA_C_CS")) : 0;
+    }
+    // 16-bit C by TMA stores from shared-memory staging (the instantiations
+    // with a staging area: CTA pairs, no producer-fused combine, QF 0)
+    g.c_tma = 0;
+    const bool has_stage = f8 || !regh || dyn || cst_regh;
+    if (has_stage && g.out_type != OUT_FP32 && p->cg == 2 && !pf && !qf && !H && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
+        (g.ldc * 2) % 16 == 0 && !(diag_env("LCMA_C_TMA") && std::atoi(diag_env("LCMA_C_TMA")) == 0)) {
+        const CUtensorMapDataType ct = g.out_type == OUT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+        if (make_map_t(&g.c_map, C, ct, 2, (uint64_t)p->d.N, (uint64_t)p->d.M * p->nbatch, 32, 32,
+                       CU_TENSOR_MAP_SWIZZLE_NONE) == LCMA_OK)
+            g.c_tma = 1;
+        else
+            t_err.clear();
     }
     if (const char* dbg = diag_env("LCMA_DEBUG")) g.debug = std::atoi(dbg);
     // fused Combine H partials carry an L2 evict_last policy (measured: -1 %
@@ -1141,9 +1165,10 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         cfg.dynamicSmemBytes = Cfg<2, 256, 1>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 1, true>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256 && regh) {
-        cfg.dynamicSmemBytes = Cfg<2, 256>::kSmemBytes;
+        cfg.dynamicSmemBytes = (dyn || cst_regh) ? Cfg<2, 256>::kSmemBytes : Cfg<2, 256, 0, false, 0, false, false>::kSmemBytes;
         e = dyn ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 0, true>, ta, tb, g)
-                : cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true>, ta, tb, g);
+            : cst_regh ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true>, ta, tb, g)
+                       : cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 0, false, false, false>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256) {
         cfg.dynamicSmemBytes = Cfg<2, 256, 0, true>::kSmemBytes;
         e = dyn ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, false, 0, true>, ta, tb, g)

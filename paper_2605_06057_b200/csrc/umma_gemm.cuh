@@ -75,7 +75,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // F8: FP8 E4M3 operands (128 elements per 128-byte row) plus, per stage, the
 // 512-byte UE8M0 scale chunks of the A rows and of the B columns (1 x 128
 // block scaling, reading 23).
-template <int CG, int BN = kBN, int QF = 0, bool NP = false, int PF = 0, bool F8 = false>
+// CST: C staging area for TMA stores (costs one operand stage in the
+// register-home instantiation; the long-K variant keeps the stage instead)
+template <int CG, int BN = kBN, int QF = 0, bool NP = false, int PF = 0, bool F8 = false, bool CST = true>
 struct Cfg {
     static constexpr int kTileM = kBM * CG;                  // rows per group tile
     static constexpr int kBNc = BN / CG;                     // B columns staged per CTA
@@ -92,9 +94,12 @@ struct Cfg {
     static constexpr int kMaxStages = F8 ? 8 : (NP ? LCMA_MAX_STAGES_NP : LCMA_MAX_STAGES);
     // as many stages as fit in 227 KB (minus the partial, alignment slack and
     // barriers), <= LCMA_MAX_STAGES
-    static constexpr int kFree = 232448 - 1024 - kBarBytes - kPartialSmem;
+    // C staging for TMA stores of 16-bit C (GemmParams::c_tma): two 32 x 32
+    // 16-bit boxes (2 KB each) per epilogue warp
+    static constexpr int kCStage = (CST && CG == 2 && PF == 0 && QF == 0) ? kEpiWarps * 2 * 2048 : 0;
+    static constexpr int kFree = 232448 - 1024 - kBarBytes - kPartialSmem - kCStage;
     static constexpr int kStages = (kFree / kStageBytes) > kMaxStages ? kMaxStages : (kFree / kStageBytes);
-    static constexpr int kSmemBytes = kStages * kStageBytes + kPartialSmem + 1024 /*align*/ + kBarBytes;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kPartialSmem + kCStage + 1024 /*align*/ + kBarBytes;
 };
 
 // The 256-column pair kernel without a register home is only launched for
@@ -105,8 +110,8 @@ struct KernelNP {
     static constexpr bool value = CG == 2 && (BN == 256 || F8) && QF == 0 && !REGH;
 };
 // the shared-memory configuration of umma_gemm_kernel<CG, BN, QF, REGH, PF, DYN, F8>
-template <int CG, int BN, int QF, bool REGH, int PF, bool F8>
-using KernelCfg = Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH, F8>::value, PF, F8>;
+template <int CG, int BN, int QF, bool REGH, int PF, bool F8, bool CST = true>
+using KernelCfg = Cfg<CG, BN, QF, KernelNP<CG, BN, QF, REGH, F8>::value, PF, F8, CST>;
 
 enum EpiMode : int { EPI_FUSED = 0, EPI_STORE_H = 1 };
 enum OutType : int { OUT_BF16 = 0, OUT_FP16 = 1, OUT_FP32 = 2 };
@@ -122,6 +127,12 @@ struct GemmParams {
     alignas(64) CUtensorMap sfa_map;
     alignas(64) CUtensorMap sfb_map;
     int sf_nkb;            // k-blocks per operand row (Kb / 128)
+    // 16-bit C written by TMA stores of 32 x 32 boxes staged in shared memory
+    // (c_tma = 1): the epilogue threads' row-per-lane stores become one
+    // asynchronous bulk store per warp and chunk; rows >= M / columns >= N
+    // are clipped by the map ({N, M * nbatch})
+    alignas(64) CUtensorMap c_map;
+    int c_tma;
     // problem / blocking
     int nX, nZ;            // group tiles along M, N: Mb/kTileM, Nb/kBN
     int G;                 // groups = nX * nZ
@@ -171,7 +182,7 @@ struct GemmParams {
     int c_cs;              // streaming (evict-first) C stores
     void* C;
     float* P;              // partial tiles (see partial_tile), each [kBN/4][kBM][4] fp32
-    int* flags;            // [ctas] split-segment ready flags
+    int* flags;            // [2 ctas] split-segment ready flags (contributor units, owner units)
     float* H;              // EPI_STORE_H: H [R][Mb][Nb] fp32
     int discard;           // 1: discard.global.L2 partial lines after their last read
     int pace_ns;           // >0: sleep between C_ij updates (spreads epilogue traffic)
@@ -634,19 +645,22 @@ __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, unsig
 }
 
 // ------------------------------------------------------------ the kernel
-template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false, bool F8 = false>
+template <int CG, int BN, int QF = 0, bool REGH = false, int PF = 0, bool DYN = false, bool F8 = false,
+          bool CST = true>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ GemmParams p) {
-    using C_ = KernelCfg<CG, BN, QF, REGH, PF, F8>;
+    using C_ = KernelCfg<CG, BN, QF, REGH, PF, F8, CST>;
     static_assert(!F8 || (BN == 128 && PF == 0), "FP8: 128-column tiles (2 x 128 accumulator columns + scales in TMEM)");
     constexpr int kStages = C_::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     float* psmem = reinterpret_cast<float*>(smem + kStages * C_::kStageBytes);   // [QF?BN/4:BN/8][kBM][4]
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * C_::kStageBytes + C_::kPartialSmem);
+    // C staging boxes [kEpiWarps][2][32 rows][64 B] (TMA stores)
+    uint8_t* cstage = smem + kStages * C_::kStageBytes + C_::kPartialSmem;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * C_::kStageBytes + C_::kPartialSmem + C_::kCStage);
     uint64_t* empty_bar = full_bar + kStages;
     uint64_t* tfull_bar = empty_bar + kStages;   // [2]
     uint64_t* tempty_bar = tfull_bar + 2;        // [2]
@@ -742,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef LCMA_DIAG
                         // diagnostics build: the general loop below whenever a knob
                         // changes what the producer issues
-                        const bool lean = !(p.debug & (16 | 32 | 64 | 4096)) && !p.stats && !p.operand_hint;
+                        const bool lean = !(p.debug & (16 | 32 | 64 | 4096)) && !p.operand_hint;
 #else
                         constexpr bool lean = true;
 #endif
@@ -1093,7 +1107,87 @@ __global__ void __launch_bounds__(kThreads, 1)
         // classical and unfused GEMMs keep the register budget)
         constexpr int kPregCols = REGH ? BN / 2 : 1;
         float preg[kPregCols];
+        uint8_t* cst = cstage + ew * 2 * 2048;     // this warp's two C staging boxes
+        int cbuf = 0;
         int tl_i = 0;             // timeline product index (diagnostics)
+        // the static tail's merges, after the segment: wait for the group's
+        // other units, merge this unit's share of the (C_ij, 16-column slice)
+        // items in segment order, store C, count the read flags down
+        auto merge_split = [&](const int g_m, const int seg_m) {
+            int x, z;
+            group_xz(p, g_m, x, z);
+            const long long radd = p.nbatch > 1 ? (long long)(g_m / p.Gb) * p.M : 0;
+            const long long brow = (long long)x * C_::kTileM + (long long)rank * kBM + row;
+            const long long Tb = (long long)(g_m - p.n_whole) * p.R;      // tail-local first tile
+            const int s0 = (int)(Tb / p.tail_c), s1 = (int)((Tb + p.R - 1) / p.tail_c);
+            const int nseg = s1 - s0 + 1;
+            const int me = seg_m - s0;
+            auto fidx = [&](int v) { return (v == s0 ? (int)gridDim.x : 0) + v * CG + (int)rank; };
+            if (ew == 0 && lane == 0) {
+                for (int v = s0; v <= s1; ++v) {
+                    if (v == seg_m) continue;
+                    int f = 0;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.flags + fidx(v)) : "memory");
+                    } while (f <= 0);
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+            constexpr int kSl = (BN / 2) / 16;                              // 16-column slices per thread
+            for (int ij = 0; ij < mn; ++ij) {
+                const int i = ij / p.n, j = ij - (ij / p.n) * p.n;
+                for (int ch = 0; ch < kSl; ++ch) {
+                    if ((ij * kSl + ch) % nseg != me) continue;
+                    const int col0 = half * (BN / 2) + ch * 16;
+                    float v[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                    int vs = s0;
+                    for (;;) {
+                        // next batch of up to 4 units that touch C_ij, in order
+                        int src[4];
+                        int ns = 0;
+                        for (; vs <= s1 && ns < 4; ++vs) {
+                            const long long lo_t = (long long)vs * p.tail_c > Tb ? (long long)vs * p.tail_c : Tb;
+                            const long long hi_t = (long long)(vs + 1) * p.tail_c < Tb + p.R ? (long long)(vs + 1) * p.tail_c
+                                                                                            : Tb + p.R;
+                            bool touch = false;
+                            for (long long t = lo_t; t < hi_t && !touch; ++t)
+                                touch = p.Wc[p.rperm[(int)(t - Tb)] * mn + ij] != 0;
+                            if (touch) src[ns++] = (vs == s0 ? 0 : (int)gridDim.x) + vs * CG + (int)rank;
+                        }
+                        if (ns == 0) break;
+                        float4 o[4][4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float* pt = partial_tile<BN>(p, q < ns ? src[q] : src[0], ij, false);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) o[q][e] = ld_cg_f4(pt + partial_off(row, (col0 >> 2) + e));
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            if (q < ns) {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    v[4 * e] += o[q][e].x; v[4 * e + 1] += o[q][e].y;
+                                    v[4 * e + 2] += o[q][e].z; v[4 * e + 3] += o[q][e].w;
+                                }
+                            }
+                        }
+                        if (ns < 4) break;
+                    }
+                    const long long ccol = (long long)j * p.Nb + (long long)z * BN + col0;
+                    if (brow < p.Mb && ccol < (long long)(j + 1) * p.Nb)
+                        store_c_row16(p, (long long)i * p.Mb + brow, ccol, v, radd);
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+            if (ew == 0 && lane == 0)
+                for (int v = s0; v <= s1; ++v)
+                    if (v != seg_m) atomicSub(p.flags + fidx(v), 1);
+        };
+        int pend_g[2] = {-1, -1};
+        int npend = 0;
         UnitIter<DYN> it(p, w, ring, leader ? SR_LOCAL : SR_PEER, CG);
         Unit u;
         while (it.next(u)) {
@@ -1125,11 +1219,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // same product (each thread touches only its own elements)
                 const uint32_t fin = whole ? (nz & ~later) : 0u;
                 const int col_base = half * (BN / 2);
+                // first C row of this warp's 32-row box (TMA-store path)
+                const long long box_row = (long long)x * C_::kTileM + (long long)rank * kBM + quarter * 32 + radd;
                 // the accumulator is consumed in chunks of 32 columns; it is
                 // released to the MMA warp right after the last chunk's load.
                 // The chunk index is a template constant so that the register
                 // partial preg is indexed statically (stays in registers).
-                auto chunk = [=, &preg, &p](auto ch_c) {
+                auto chunk = [=, &preg, &p, &cbuf](auto ch_c) {
+                    // 16-bit C through shared memory and a TMA store: this lane's 16
+                    // values at column half hh of the warp's current 32 x 32 box
+                    auto c_stage16 = [&](int hh, const float* v) {
+                        uint32_t wv[8];
+#pragma unroll
+                        for (int h = 0; h < 8; ++h) wv[h] = pack2(p, v[2 * h], v[2 * h + 1]);
+                        uint4* dst = reinterpret_cast<uint4*>(cst + cbuf * 2048 + lane * 64 + hh * 32);
+                        dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                        dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                    };
+                    // the warp's box is complete: one bulk store (rows >= M, columns
+                    // >= N clipped by the map), then the other box; it is reused once
+                    // the store issued before this one has read it
+                    auto c_flush = [&](int i_blk, long long ccol) {
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_2d(&p.c_map, cst + cbuf * 2048, (int)ccol, (int)((long long)i_blk * p.Mb + box_row));
+                            ptx::bulk_commit_group();
+                            ptx::bulk_wait_group_read<1>();
+                        }
+                        cbuf ^= 1;
+                        __syncwarp();
+                    };
                     constexpr int ch = decltype(ch_c)::value;
                     uint32_t raw[32];
                     if (!(p.debug & 2)) {
@@ -1187,8 +1307,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     for (int e = 0; e < 32; ++e)
                                         pr[e] = (first ? 0.f : pr[e]) + sw * __uint_as_float(raw[e]);
                                     if (in_range && !(p.debug & 128)) {
-                                        store_c_row16(p, (long long)i * p.Mb + brow, ccol, pr, radd);
-                                        store_c_row16(p, (long long)i * p.Mb + brow, ccol + 16, pr + 16, radd);
+                                        if (p.c_tma) {
+                                            c_stage16(0, pr);
+                                            c_stage16(1, pr + 16);
+                                            c_flush(i, ccol);
+                                        } else {
+                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol, pr, radd);
+                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol + 16, pr + 16, radd);
+                                        }
                                     }
                                 } else if (first) {
 #pragma unroll
@@ -1215,9 +1341,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             v[e + 2] = o.z + sw * __uint_as_float(raw[hh + e + 2]);
                                             v[e + 3] = o.w + sw * __uint_as_float(raw[hh + e + 3]);
                                         }
-                                        if (in_range && !(p.debug & 128))
-                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v, radd);
+                                        if (in_range && !(p.debug & 128)) {
+                                            if (p.c_tma) c_stage16(hh >> 4, v);
+                                            else store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v, radd);
+                                        }
                                     }
+                                    if (p.c_tma && in_range && !(p.debug & 128)) c_flush(i, ccol);
                                 } else {
 #pragma unroll
                                     for (int e = 0; e < 32; e += 4) {
@@ -1253,9 +1382,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                 v[4 * q + 2] += o[q].z; v[4 * q + 3] += o[q].w;
                                             }
                                         }
-                                        if (in_range && !(p.debug & 128))
-                                            store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v, radd);
+                                        if (in_range && !(p.debug & 128)) {
+                                            if (p.c_tma) c_stage16(hh >> 4, v);
+                                            else store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v, radd);
+                                        }
                                     }
+                                    if (p.c_tma && in_range && !(p.debug & 128)) c_flush(i, ccol);
                                     if (!first && p.discard) {
                                         __syncwarp();      // the 8 lanes sharing a line have read it
                                         if ((row & 7) == 0) discard_lines(pt, row, c4, 8);
@@ -1303,6 +1435,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 seen |= nz;
             }
             if (p.epi_mode != EPI_FUSED || u.role == ROLE_WHOLE || (p.debug & 1)) continue;
+
+            if constexpr (!DYN) {
+                // ---- split group, static tail (segment v runs on pair v): every
+                // unit of a split group publishes its partials right after its
+                // products (no wait here: a wait inside the segment would chain
+                // the pairs), the merges run once the whole segment is done
+                // (merge_split below).  Flags count down: a unit sets nseg - 1,
+                // every reader decrements once after its reads, so they are zero
+                // again at the end of the launch.  flags: [0, ctas) contributor
+                // units, [ctas, 2 ctas) owner units.
+                const long long Tb = (long long)(u.g - p.n_whole) * p.R;
+                const int s0 = (int)(Tb / p.tail_c), s1 = (int)((Tb + p.R - 1) / p.tail_c);
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+                if (ew == 0 && lane == 0)
+                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flags + (u.seg == s0 ? (int)gridDim.x : 0) +
+                                                                             u.seg * CG + (int)rank),
+                                 "r"(s1 - s0) : "memory");
+                if (npend < 2) pend_g[npend++] = u.g;
+                continue;
+            }
 
             // ---- split group: publish (contributor) or merge (owner)
             if (u.role == ROLE_CONTRIB) {
@@ -1409,10 +1562,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (ew == 0 && lane == 0)
                 for (int v = u.seg + 1; v <= last_w; ++v) p.flags[v * CG + rank] = 0;
         }
+        if constexpr (!DYN) {
+            // static tail: the segment's split units are merged after all of them
+            // published (segment v = unit v, the pair's last work)
+            for (int q = 0; q < npend; ++q) merge_split(pend_g[q], w);
+        }
         if (p.stats && ew == 0 && lane == 0) {
             p.stats[blockIdx.x * kStatsPerCta + 4] = w_tfull;
             (void)t_epi0;
         }
+        if (p.c_tma && lane == 0) ptx::bulk_wait_group_all();   // staging stays valid until read
     }
 
     ptx::tc_fence_before();
