@@ -27,6 +27,7 @@ struct CombineParams {
     int elem;                 // ElemType
     int round_tf32;           // fp32 outputs rounded RN-away to tf32
     int8_t coef[kCombMaxR * kCombMaxPQ];   // coef[r][p*Q + q]
+    uint8_t skip[kCombMaxR];  // 1: output r not written (a single +1 source block the GEMM reads in place)
 };
 
 template <int VEC>
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(256, 4) group_combine16_kernel(const __grid_co
             }
         }
         for (int r = 0; r < p.R; ++r) {
+            if (p.skip[r]) continue;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (v0 + u >= nvec) continue;
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(256) group_combine_kernel(const __grid_constan
             load_vec<VEC>(p, pi * p.E0 + e0, qi * p.E1 + e1, src[pq]);
         }
         for (int r = 0; r < p.R; ++r) {
+            if (p.skip[r]) continue;
             float acc[VEC];
 #pragma unroll
             for (int e = 0; e < VEC; ++e) acc[e] = 0.f;

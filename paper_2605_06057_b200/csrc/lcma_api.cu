@@ -116,6 +116,8 @@ struct lcma_plan_s {
     int nbatch = 1;                // batched inner GEMMs of a two-level plan (groups = nbatch x nX x nZ)
     size_t off_sched, off_P, off_flags, off_At, off_Bt, off_H, ws_bytes, bt_bytes;
     size_t off_inner = 0;          // two-level: the inner plan's partial slots + flags
+    int8_t a_dir[kMaxR], b_dir[kMaxR];   // single-term operands read in place (-1: materialised)
+    bool any_a_dir = false, any_b_dir = false;
     lcma_plan_s* inner = nullptr;  // two-level: fused GEMM plan of the base scheme
     lcma_plan_info info;
     ~lcma_plan_s() { delete inner; }
@@ -463,6 +465,26 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         }
     }
     p->ws_bytes = off;
+    // single +1-term combined operands read in place by the fused GEMM (16-bit
+    // data, block grid tiling M, K (and N for B, stored N x K) exactly)
+    for (int r = 0; r < kMaxR; ++r) p->a_dir[r] = p->b_dir[r] = -1;
+    if (!classical && variant == LCMA_VARIANT_FUSED_H && (d.dtype == LCMA_BF16 || d.dtype == LCMA_FP16) &&
+        S.R <= kMaxR && p->cg == 2 && p->bn == 256) {
+        const bool a_ok = d.M == (int64_t)S.m * p->Mb && d.K == (int64_t)S.k * p->Kb;
+        const bool b_ok = d.b_layout == 1 && d.N == (int64_t)S.n * p->Nb && d.K == (int64_t)S.k * p->Kb;
+        for (int r = 0; r < S.R; ++r) {
+            int nz = 0, blk = -1, val = 0;
+            for (int a = 0; a < S.m; ++a)
+                for (int b = 0; b < S.k; ++b)
+                    if (S.u(r, a, b)) { ++nz; blk = a * S.k + b; val = S.u(r, a, b); }
+            if (a_ok && nz == 1 && val == 1) { p->a_dir[r] = (int8_t)blk; p->any_a_dir = true; }
+            nz = 0; blk = -1; val = 0;
+            for (int l = 0; l < S.k; ++l)
+                for (int j = 0; j < S.n; ++j)
+                    if (S.v(r, l, j)) { ++nz; blk = j * S.k + l; val = S.v(r, l, j); }
+            if (b_ok && nz == 1 && val == 1) { p->b_dir[r] = (int8_t)blk; p->any_b_dir = true; }
+        }
+    }
     p->bt_bytes = fp8 ? fp8_operand_bytes(S.R, p->Nb, p->Kb) : classical ? 0 : (size_t)S.R * p->Kb * p->Nb * e;
 
     // ---- info
@@ -757,7 +779,7 @@ int grid_for(long long work, int per_block) {
 
 // Group combine of one operand into dst[R][E0][E1] (Alg. 2 stage 1 or 2).
 lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, bool is_b,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool direct = false) {
     const Scheme& S = p->sch;
     CombineParams c;
     std::memset(&c, 0, sizeof(c));
@@ -766,6 +788,8 @@ lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, boo
     c.R = S.R;
     c.elem = p->d.dtype == LCMA_BF16 ? ELEM_BF16 : p->d.dtype == LCMA_FP16 ? ELEM_FP16 : ELEM_FP32;
     c.round_tf32 = p->d.dtype == LCMA_TF32;
+    if (direct)   // outputs the GEMM reads in place (single +1 source block)
+        for (int r = 0; r < S.R && r < kCombMaxR; ++r) c.skip[r] = (is_b ? p->b_dir[r] : p->a_dir[r]) >= 0;
     int P, Q;
     if (!is_b) {                      // A (M x K): blocks (i, l), coef U[r][i][l]
         c.rows = p->d.M; c.cols = p->d.K; c.E0 = p->Mb; c.E1 = p->Kb; P = S.m; Q = S.k;
@@ -883,7 +907,8 @@ lcma_status launch_combine_h(const lcma_plan_s* p, const float* H, void* C, cuda
 // tcgen05 GEMM: classical (R == 1 over A, B) or the LCMA GEMM stage over the
 // materialised At / Bt with the fused Combine H (or H store) epilogue.
 lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, void* C, float* P,
-                        int* flags, int* sched, float* H, cudaStream_t st, int pf = 0) {
+                        int* flags, int* sched, float* H, cudaStream_t st, int pf = 0,
+                        const void* Araw = nullptr, const void* Braw = nullptr) {
     const Scheme& S = p->sch;
     const bool classical = p->scheme_id == SCHEME_CLASSICAL;
     // QF: the shared-memory partial home covers both column halves (3 operand
@@ -1024,6 +1049,27 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         else
             t_err.clear();
     }
+    g.pf_kb = 0;
+    // in-place single-term operands (lean producer path only; the diagnostics
+    // build takes the general loop when a producer knob is set)
+    g.use_dir = 0;
+    for (int r = 0; r < kMaxR; ++r) g.a_dir[r] = g.b_dir[r] = -1;
+    if (Araw || Braw) {   // run() decided (direct_ok): the combines skipped these outputs
+        if (Araw) {
+            rs = make_map(&g.a_raw, Araw, dt, p->d.K, p->d.M, epr, kBM);
+            if (rs != LCMA_OK) return rs;
+            for (int r = 0; r < S.R; ++r) g.a_dir[r] = p->a_dir[r];
+        }
+        if (Braw) {
+            rs = make_map(&g.b_raw, Braw, dt, p->d.K, p->d.N, epr, p->bn / p->cg);
+            if (rs != LCMA_OK) return rs;
+            for (int r = 0; r < S.R; ++r) g.b_dir[r] = p->b_dir[r];
+        }
+        g.use_dir = 1;
+        g.kgrid = S.k;
+        g.pf_Kb = (int)p->Kb;
+    }
+    if (const char* v = diag_env("LCMA_PFKB")) g.pf_kb = std::atoi(v);
     if (const char* dbg = diag_env("LCMA_DEBUG")) g.debug = std::atoi(dbg);
     // fused Combine H partials carry an L2 evict_last policy (measured: -1 %
     // at cfg2, -3..7 % at the cfg5 shard; profiles/r01b_l2_residency.txt)
@@ -1210,6 +1256,17 @@ lcma_status launch_simt(const lcma_plan_s* p, const float* A, const float* B, fl
     return check_launch("simt_sgemm_batched_kernel");
 }
 
+// In-place single-term operands apply to the fused (FUSED_H) GEMM through
+// its lean producer loop: not in diagnostics runs whose knobs change what the
+// producer issues (the general loop does not read in place).
+bool direct_ok(const lcma_plan_s* p) {
+    if (p->variant != LCMA_VARIANT_FUSED_H || p->nbatch != 1 || p->d.b_layout != 1) return false;
+    if (diag_env("LCMA_DEBUG") && (std::atoi(diag_env("LCMA_DEBUG")) & (16 | 32 | 64 | 4096))) return false;
+    if (diag_env("LCMA_OPERAND_HINT")) return false;
+    if (diag_env("LCMA_DIRECT") && std::atoi(diag_env("LCMA_DIRECT")) == 0) return false;
+    return true;
+}
+
 bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
     auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
     return na && nb && x < y + nb && y < x + na;
@@ -1262,8 +1319,11 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
     void* At = w + p->off_At;
     const void* Bt = Bt_user;
     lcma_status rs = LCMA_OK;
+    const bool dir = direct_ok(p);
+    const bool dirA = dir && p->any_a_dir;
+    const bool dirB = dir && p->any_b_dir && !Bt_user && B;
     if (p->variant != LCMA_VARIANT_PRODUCER) {
-        rs = launch_combine(p, A, At, false, st);                  // Combine A (Eq. 3)
+        rs = launch_combine(p, A, At, false, st, dirA);            // Combine A (Eq. 3)
         if (rs != LCMA_OK) return rs;
     }
     // variant 3: Combine B joins Combine A in the producer path when B is
@@ -1283,7 +1343,7 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
         if (two) pf = 2;
     }
     if (!Bt && pf != 2) {
-        rs = launch_combine(p, B, w + p->off_Bt, true, st);        // Combine B (Eq. 4)
+        rs = launch_combine(p, B, w + p->off_Bt, true, st, dirB);  // Combine B (Eq. 4)
         if (rs != LCMA_OK) return rs;
         Bt = w + p->off_Bt;
     }
@@ -1324,7 +1384,7 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
                            reinterpret_cast<int*>(w + p->off_flags), nullptr, nullptr, st, pf);
     return launch_umma(p, At, Bt, C, reinterpret_cast<float*>(w + p->off_P),
                        reinterpret_cast<int*>(w + p->off_flags), reinterpret_cast<int*>(w + p->off_sched), nullptr,
-                       st);
+                       st, 0, dirA ? A : nullptr, dirB ? B : nullptr);
 }
 
 }  // namespace

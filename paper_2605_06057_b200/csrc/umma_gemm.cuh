@@ -127,6 +127,15 @@ struct GemmParams {
     alignas(64) CUtensorMap sfa_map;
     alignas(64) CUtensorMap sfb_map;
     int sf_nkb;            // k-blocks per operand row (Kb / 128)
+    int pf_kb;             // k-blocks of the next product prefetched to L2 at a product start (0: off)
+    // single-term combined operands read in place (A~_r = A_il, B~_r = B_lj with
+    // a +1 coefficient, exactly tiled extents): a_dir[r] = i * k + l (-1: the
+    // materialised A~_r), b_dir[r] = j * k + l; a_raw / b_raw map A (M x K) and
+    // B (N x K).  The combine kernels skip those outputs (2/7 of Strassen's).
+    alignas(64) CUtensorMap a_raw;
+    alignas(64) CUtensorMap b_raw;
+    int8_t a_dir[kMaxR], b_dir[kMaxR];
+    int use_dir;
     // 16-bit C written by TMA stores of 32 x 32 boxes staged in shared memory
     // (c_tma = 1): the epilogue threads' row-per-lane stores become one
     // asynchronous bulk store per warp and chunk; rows >= M / columns >= N
@@ -771,14 +780,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int nk = p.nK;
                             [[maybe_unused]] const int ca0 = (a_row >> 7) * p.sf_nkb;
                             [[maybe_unused]] const int cb0 = ((r * p.b_rows_per_r + z * BN) >> 7) * p.sf_nkb;
+                            if (p.pf_kb > 0 && t + 1 < u.r1) {
+                                // product boundary: the next product's first k-blocks to L2
+                                // while this one streams (its panels are new to the round)
+                                const int rn = product_at(p, u, t + 1) + qb * p.R;
+                                const int an = rn * p.a_rows_per_r + x * C_::kTileM + (int)rank * kBM;
+                                const int bn = rn * p.b_rows_per_r + b_col0;
+                                const int np = p.pf_kb < nk ? p.pf_kb : nk;
+                                for (int q = 0; q < np; ++q) {
+                                    ptx::tma_prefetch_2d(&tmap_a, q * (F8 ? 128 : p.BK), an);
+                                    ptx::tma_prefetch_2d(&tmap_b, q * (F8 ? 128 : p.BK), bn);
+                                }
+                            }
+                            // in-place operands (p.a_dir / p.b_dir): the source block's rows
+                            // and column offset inside A (B)
+                            const CUtensorMap* ma = &tmap_a;
+                            const CUtensorMap* mb = &tmap_b;
+                            int ar = a_row, br = b_row, ak0 = 0, bk0 = 0;
+                            if (!F8 && p.use_dir) {
+                                const int da = p.a_dir[r], db = p.b_dir[r];
+                                if (da >= 0) {
+                                    ma = &p.a_raw;
+                                    ar = (da / p.kgrid) * (int)p.Mb + x * C_::kTileM + (int)rank * kBM;
+                                    ak0 = (da % p.kgrid) * p.pf_Kb;
+                                }
+                                if (db >= 0) {
+                                    mb = &p.b_raw;
+                                    br = (db / p.kgrid) * (int)p.Nb + b_col0;
+                                    bk0 = (db % p.kgrid) * p.pf_Kb;
+                                }
+                            }
                             for (int kb = 0; kb < nk; ++kb) {
                                 ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                                 uint8_t* sa = smem + stage * C_::kStageBytes;
                                 const uint32_t lbar = lbar0 + 8u * (uint32_t)stage;
                                 if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kStageBytes * CG);
                                 const int kcol = kb * (F8 ? 128 : p.BK);
-                                ptx::tma_load_2d_cg2(sa, &tmap_a, lbar, kcol, a_row);
-                                ptx::tma_load_2d_cg2(sa + C_::kABytes, &tmap_b, lbar, kcol, b_row);
+                                ptx::tma_load_2d_cg2(sa, ma, lbar, ak0 + kcol, ar);
+                                ptx::tma_load_2d_cg2(sa + C_::kABytes, mb, lbar, bk0 + kcol, br);
                                 if constexpr (F8) {
                                     ptx::tma_load_2d_cg2(sa + C_::kABytes + C_::kBBytes, &p.sfa_map, lbar, 0,
                                                          2 * (ca0 + kb));
