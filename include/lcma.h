@@ -122,7 +122,7 @@ typedef struct {
     int32_t b_layout;         /* 0: B is K x N (paper), 1: B is N x K              */
     int32_t b_static;         /* 1: lcma_gemm_precombined will be used     */
     int32_t variant;          /* lcma_variant                                      */
-    int32_t schedule;         /* 0 auto = 1; 1 = 4: cache-aware lockstep rounds
+    int32_t schedule;         /* 0 auto (classical 5, LCMA 1); 1 = 4: cache-aware lockstep rounds
                                  (group w + i*W to unit w) + split tail;
                                  2 paper's contiguous split-group order;
                                  3 whole groups only (group-parallel, no split);
@@ -131,7 +131,9 @@ typedef struct {
                                    in flight stay a compact window of the raster)
                                    + the split tail's segments handed out at run
                                    time to the pairs that finish first;
-                                 6 static lockstep rounds + the run-time tail      */
+                                 6 static lockstep rounds + the run-time tail;
+                                 7 whole groups at run time (as 5) + the static
+                                   tail, merged by all of a split group's pairs */
     int32_t num_ctas;         /* 0 = one per SM                                    */
     const lcma_hw_profile* hw;/* NULL -> built-in B200 profile                     */
     int32_t decision_model;   /* algo AUTO: 0 = this build's B200-calibrated model

@@ -169,9 +169,11 @@ void make_schedule(lcma_plan_s* p, int mode) {
         // reads at the cfg5 shape, but measured no faster: within +-1 % at
         // cfg2, -8..-16 % (classical) / -2..+9 % (Strassen) at cfg5,
         // profiles/r02_schedule.txt), so the default (1 = 4) stays static
-        p->dyn = mode == 5 ? 1 : 0;
+        p->dyn = (mode == 5 || mode == 7) ? 1 : 0;
         // modes 5 and 6: the split tail's segments are handed out at run time
-        // to the pairs that finish their whole groups first
+        // to the pairs that finish their whole groups first; mode 7: whole
+        // groups at run time, the static tail (segment w on pair w, merged by
+        // all of a group's pairs)
         p->dyn_tail = (mode == 5 || mode == 6) ? 1 : 0;
     }
     p->n_whole = (int)std::min<long long>((long long)p->q * W, p->G);
@@ -371,7 +373,12 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
             return fail(LCMA_ERR_NOT_SUPPORTED, "problem too large for 32-bit tile coordinates");
         }
         p->G = p->nX * p->nZ;
-        make_schedule(p, (d.schedule >= 2 && d.schedule <= 6) ? d.schedule : 1);
+        // default (0): the classical kernel hands its groups out at run time
+        // (schedule 5: the lockstep pairs drift apart; measured +2.6..5.4 %
+        // over the static rounds at cfg2 / cfg4 / cfg5 with the lean producer,
+        // tools/r02/sched7.sh), LCMA plans keep the static lockstep rounds
+        // (r-aligned products; the run-time hand-out measured 2-13 % slower)
+        make_schedule(p, (d.schedule >= 1 && d.schedule <= 7) ? d.schedule : (classical ? 5 : 1));
         // the dynamic schedule is instantiated for the 256-column pair kernels
         // (classical and fused Combine H); the producer-fused variant's
         // combine warps walk the static schedule
@@ -416,7 +423,7 @@ extern "C" lcma_status lcma_plan_ex(const lcma_plan_desc* desc, lcma_plan_t* out
         // enough groups per launch for the persistent grid
         in->nbatch = B0.R;
         in->G = in->nX * in->nZ * in->nbatch;
-        make_schedule(in, (d.schedule >= 2 && d.schedule <= 6) ? d.schedule : 1);
+        make_schedule(in, (d.schedule >= 2 && d.schedule <= 7) ? d.schedule : 1);
         if ((in->dyn || in->dyn_tail) && (in->cg != 2 || in->bn != 256)) make_schedule(in, 1);
         p->inner = in;
     }
@@ -936,7 +943,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
                    : pf == 1 ? ensure_smem_attr<2, 256, 0, true, 1>()
                    : p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
                                                 : (qf ? ensure_smem_attr<2, 256, 1, true>()
-                                                      : regh ? (dyn ? ensure_smem_attr<2, 256, 0, true, 0, true>()
+                                                      : regh ? (dyn ? (cst_regh ? ensure_smem_attr<2, 256, 0, true, 0, true>()
+                                                                          : ensure_smem_attr<2, 256, 0, true, 0, true, false, false>())
                                                                     : cst_regh ? ensure_smem_attr<2, 256, 0, true>()
                                                                     : ensure_smem_attr<2, 256, 0, true, 0, false, false, false>())
                                                              : (dyn ? ensure_smem_attr<2, 256, 0, false, 0, true>()
@@ -1038,7 +1046,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     // 16-bit C by TMA stores from shared-memory staging (the instantiations
     // with a staging area: CTA pairs, no producer-fused combine, QF 0)
     g.c_tma = 0;
-    const bool has_stage = f8 || !regh || dyn || cst_regh;
+    const bool has_stage = f8 || !regh || cst_regh;
     if (has_stage && g.out_type != OUT_FP32 && p->cg == 2 && !pf && !qf && !H && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
         (g.ldc * 2) % 16 == 0 && !(diag_env("LCMA_C_TMA") && std::atoi(diag_env("LCMA_C_TMA")) == 0)) {
         const CUtensorMapDataType ct = g.out_type == OUT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -1211,8 +1219,9 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         cfg.dynamicSmemBytes = Cfg<2, 256, 1>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 1, true>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256 && regh) {
-        cfg.dynamicSmemBytes = (dyn || cst_regh) ? Cfg<2, 256>::kSmemBytes : Cfg<2, 256, 0, false, 0, false, false>::kSmemBytes;
-        e = dyn ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 0, true>, ta, tb, g)
+        cfg.dynamicSmemBytes = cst_regh ? Cfg<2, 256>::kSmemBytes : Cfg<2, 256, 0, false, 0, false, false>::kSmemBytes;
+        e = dyn ? (cst_regh ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 0, true>, ta, tb, g)
+                            : cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 0, true, false, false>, ta, tb, g))
             : cst_regh ? cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true>, ta, tb, g)
                        : cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 0, false, false, false>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256) {

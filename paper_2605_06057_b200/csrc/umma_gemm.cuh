@@ -1475,7 +1475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (p.epi_mode != EPI_FUSED || u.role == ROLE_WHOLE || (p.debug & 1)) continue;
 
-            if constexpr (!DYN) {
+            if (!DYN || !p.dyn_tail) {
                 // ---- split group, static tail (segment v runs on pair v): every
                 // unit of a split group publishes its partials right after its
                 // products (no wait here: a wait inside the segment would chain
@@ -1601,7 +1601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (ew == 0 && lane == 0)
                 for (int v = u.seg + 1; v <= last_w; ++v) p.flags[v * CG + rank] = 0;
         }
-        if constexpr (!DYN) {
+        if (!DYN || !p.dyn_tail) {
             // static tail: the segment's split units are merged after all of them
             // published (segment v = unit v, the pair's last work)
             for (int q = 0; q < npend; ++q) merge_split(pend_g[q], w);

@@ -411,7 +411,7 @@ def test_partial_homes_exact_diag_build():
     assert "homes ok" in r.stdout
 
 
-@pytest.mark.parametrize("schedule", [1, 5, 6])
+@pytest.mark.parametrize("schedule", [1, 5, 6, 7])
 @pytest.mark.parametrize("algo,shape,ctas", [("strassen", (1536, 2304, 512), 0), ("strassen", (1536, 2304, 512), 10),
                                              ("strassen", (2560, 3072, 256), 6), ("laderman", (1000, 808, 520), 4),
                                              ("classical", (2304, 2560, 256), 8), ("classical", (1000, 1048, 520), 0)])
