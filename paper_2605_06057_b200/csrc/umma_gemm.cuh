@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #else
                         constexpr bool lean = true;
 #endif
-                        if (lean && !p.b_mn_major) {
+                        if (lean && (!p.b_mn_major || p.b_3d)) {
                             // lean issue loop (K-major A and B, the product build): per
                             // stage one wait, one expect_tx and the TMA issues with
                             // every per-product term hoisted -- at 128-deep E4M3
@@ -817,7 +817,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kStageBytes * CG);
                                 const int kcol = kb * (F8 ? 128 : p.BK);
                                 ptx::tma_load_2d_cg2(sa, ma, lbar, ak0 + kcol, ar);
-                                ptx::tma_load_2d_cg2(sa + C_::kABytes, mb, lbar, bk0 + kcol, br);
+                                if (!p.b_mn_major)
+                                    ptx::tma_load_2d_cg2(sa + C_::kABytes, mb, lbar, bk0 + kcol, br);
+                                else   // B stored K x N: one 3-D box {128 B, BK rows, BN/CG/BK chunks}
+                                    ptx::tma_load_3d_cg2(sa + C_::kABytes, &tmap_b, lbar, 0, r * p.b_rows_per_r + kcol,
+                                                         b_col0 / p.BK);
                                 if constexpr (F8) {
                                     ptx::tma_load_2d_cg2(sa + C_::kABytes + C_::kBBytes, &p.sfa_map, lbar, 0,
                                                          2 * (ca0 + kb));
