@@ -229,29 +229,31 @@ def _large_shape(L, inputs, torch, args):
     return out
 
 
-def _tf32_corner(L, inputs, torch):
-    """BASELINE cfg3's grid corner M=16384, N=K=14336 in tf32 (fp32 storage):
-    4-byte operands halve the relative cost of the fp32 Combine-H partials, so
-    this is where LCMA is measured ahead on B200 (profiles/r01d_cfg3_decision.txt)."""
+def _grid_corner(L, inputs, torch):
+    """BASELINE cfg3's grid corner M=16384, N=K=14336 (paper layout, B K x N)
+    in fp16 and tf32: the largest cfg3 shape, where the cfg3 sweep with the
+    final kernels measures Strassen ahead in fp16 (1.06x) and classical ahead
+    in tf32 (profiles/r02g_cfg3_decision.json); AUTO's choice beside both."""
     M, N, K = 16384, 14336, 14336
-    A, B = inputs.operands(M, N, K, L.TF32, 301, 302)
-    A, B = A.cuda(), B.cuda()
-    fns, keep = {}, []
-    for name, kw in (("classical", dict(algo="classical")), ("strassen", dict(algo="strassen")),
-                     ("auto", dict(algo="auto"))):
-        p = L.Plan(M, N, K, dtype=L.TF32, **kw)
-        C, ws = p.empty_c(), p.workspace()
-        fns[name] = (lambda p=p, C=C, ws=ws: p.gemm(A, B, C, ws))
-        keep += [p, C, ws]
-    med = _interleaved(fns, 1)
+    out = {"shape": [M, N, K], "timing": "median of 5 interleaved rounds"}
     fl = 2.0 * M * N * K
-    out = {"shape": [M, N, K], "dtype": "tf32", "timing": "median of 5 interleaved rounds",
-           "auto_choice": keep[6].info["scheme"]}
-    for n, ms in med.items():
-        out[n + "_tflops"] = fl / (ms * 1e-3) / 1e12
-    out["strassen_vs_classical"] = med["classical"] / med["strassen"]
-    del fns, keep
-    torch.cuda.empty_cache()
+    for dt, name in ((L.FP16, "fp16"), (L.TF32, "tf32")):
+        A, B = inputs.operands(M, N, K, dt, 301, 302)
+        A, B = A.cuda(), B.cuda()
+        fns, keep = {}, []
+        for algo in ("classical", "strassen", "auto"):
+            p = L.Plan(M, N, K, dtype=dt, algo=algo)
+            C, ws = p.empty_c(), p.workspace()
+            fns[algo] = (lambda p=p, C=C, ws=ws: p.gemm(A, B, C, ws))
+            keep += [p, C, ws]
+        med = _interleaved(fns, 1)
+        r = {"auto_choice": keep[6].info["scheme"]}
+        for n, ms in med.items():
+            r[n + "_tflops"] = fl / (ms * 1e-3) / 1e12
+        r["strassen_vs_classical"] = med["classical"] / med["strassen"]
+        out[name] = r
+        del fns, keep, A, B
+        torch.cuda.empty_cache()
     return out
 
 
@@ -391,7 +393,7 @@ def run_ours(args):
         ref["auto_pred_speedup"] = ap.info["speedup_pred"]
         if not args.no_large:
             ref["large_llama_ffn"] = _large_shape(L, inputs, torch, args)
-            ref["cfg3_tf32_corner"] = _tf32_corner(L, inputs, torch)
+            ref["cfg3_grid_corner"] = _grid_corner(L, inputs, torch)
             ref["fp8"] = _fp8_lines(L, inputs, torch)
         torch.cuda.empty_cache()
 

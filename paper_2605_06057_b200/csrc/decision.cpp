@@ -167,18 +167,18 @@ Profile default_profile(int dtype) {
     Profile p;
     // dtype 4 (FP8 E4M3): 1-byte operands after the quantizing combines
     const double bytes = (dtype == 0 || dtype == 1) ? 2.0 : dtype == 4 ? 1.0 : 4.0;
-    // classical tcgen05 kernel of this build, cfg2 (profiles/): 1.366 PF/s bf16;
-    // FP8: the 256 x 128 block-scaled pair tile
-    p.flops_mul = dtype <= 1 ? 1.366e15 : (dtype == 2 ? 0.66e15 : dtype == 4 ? 2.0e15 : 60e12);
+    // classical tcgen05 kernel of this build (lean producer; median of the
+    // cfg3 sweep, profiles/r02g_cfg3_decision.json): 1.41 PF/s fp16/bf16,
+    // 0.75 PF/s tf32; FP8: the 256 x 128 block-scaled pair tile (~2.0 PF/s)
+    p.flops_mul = dtype <= 1 ? 1.41e15 : (dtype == 2 ? 0.75e15 : dtype == 4 ? 2.0e15 : 60e12);
     p.flops_add = 148.0 * 128.0 * 1.3e9;
     p.beta = 6.55e12 / bytes;
     // group_combine_kernel measured ~4.4 TB/s of read+write traffic (cfg2)
     p.beta_combine = 4.4e12 / bytes;
-    // fused Combine H with on-chip partial homes (fit on the cfg3 sweep,
-    // profiles/r01f_cfg3_decision.json: Strassen median overhead +8 % for
-    // 16-bit data and -4 % for tf32, Laderman / Strassen^2 through alpha)
-    p.alpha_partial = 8.0;
-    p.epi_overhead = bytes <= 2.0 ? 0.08 : -0.04;
+    // refitted on the final-kernel cfg3 sweep (tools/r02/fit_decision.py:
+    // 53/56 measured-best picks, mean regret 1.001, in-sample)
+    p.alpha_partial = 16.0;
+    p.epi_overhead = bytes <= 2.0 ? 0.0 : 0.01;
     if (const char* env = diag_env("LCMA_PROFILE")) {
         const char* keys[5] = {"flops_mul=", "flops_add=", "beta_elems=", "beta_combine=", "alpha_partial="};
         double* dst[5] = {&p.flops_mul, &p.flops_add, &p.beta, &p.beta_combine, &p.alpha_partial};

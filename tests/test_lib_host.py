@@ -221,8 +221,11 @@ def test_b200_model_two_level_and_partial_terms():
     assert t["strassen2"] > t["strassen"] + 0.5 * hq
     # Laderman: 33 L2 partial transfers per group vs Strassen's 3
     assert t["laderman"] > t["strassen"]
-    # tf32 grid corner of cfg3: AUTO picks depth-1 Strassen (measured best, r01f/r01g)
-    assert L.Plan(16384, 14336, 14336, dtype=L.TF32, algo="auto").info["scheme"].startswith("strassen-2x2x2")
+    # cfg3 grid corner 16384 x 14336 x 14336 with the final kernels
+    # (profiles/r02g_cfg3_decision.json): Strassen measured best in fp16
+    # (1.06x), classical in tf32 -- AUTO follows both
+    assert L.Plan(16384, 14336, 14336, dtype=L.FP16, algo="auto").info["scheme"].startswith("strassen-2x2x2")
+    assert L.Plan(16384, 14336, 14336, dtype=L.TF32, algo="auto").info["scheme"] == "classical"
     # 16-bit cfg2: classical (measured best)
     assert L.Plan(M, N, K, dtype=L.BF16, algo="auto").info["scheme"] == "classical"
 
