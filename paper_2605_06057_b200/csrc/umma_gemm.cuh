@@ -1150,7 +1150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // classical and unfused GEMMs keep the register budget)
         constexpr int kPregCols = REGH ? BN / 2 : 1;
         float preg[kPregCols];
-        uint8_t* cst = cstage + ew * 2 * 2048;     // this warp's two C staging boxes
+        const uint32_t cst = ptx::smem_u32(cstage) + ew * 2 * 2048;   // this warp's two C staging boxes
         int cbuf = 0;
         int tl_i = 0;             // timeline product index (diagnostics)
         // the static tail's merges, after the segment: wait for the group's
@@ -1263,7 +1263,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t fin = whole ? (nz & ~later) : 0u;
                 const int col_base = half * (BN / 2);
                 // first C row of this warp's 32-row box (TMA-store path)
-                const long long box_row = (long long)x * C_::kTileM + (long long)rank * kBM + quarter * 32 + radd;
                 // the accumulator is consumed in chunks of 32 columns; it is
                 // released to the MMA warp right after the last chunk's load.
                 // The chunk index is a template constant so that the register
@@ -1275,9 +1274,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint32_t wv[8];
 #pragma unroll
                         for (int h = 0; h < 8; ++h) wv[h] = pack2(p, v[2 * h], v[2 * h + 1]);
-                        uint4* dst = reinterpret_cast<uint4*>(cst + cbuf * 2048 + lane * 64 + hh * 32);
-                        dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-                        dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                        const uint32_t dst = cst + cbuf * 2048 + lane * 64 + hh * 32;
+                        ptx::st_shared_v4(dst, wv[0], wv[1], wv[2], wv[3]);
+                        ptx::st_shared_v4(dst + 16, wv[4], wv[5], wv[6], wv[7]);
                     };
                     // the warp's box is complete: one bulk store (rows >= M, columns
                     // >= N clipped by the map), then the other box; it is reused once
@@ -1286,7 +1285,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
-                            ptx::tma_store_2d(&p.c_map, cst + cbuf * 2048, (int)ccol, (int)((long long)i_blk * p.Mb + box_row));
+                            const int brow0 = x * C_::kTileM + (int)rank * kBM + quarter * 32;
+                            ptx::tma_store_2d(&p.c_map, cst + cbuf * 2048, (int)ccol,
+                                              (int)((long long)i_blk * p.Mb + brow0 + radd));
                             ptx::bulk_commit_group();
                             ptx::bulk_wait_group_read<1>();
                         }
