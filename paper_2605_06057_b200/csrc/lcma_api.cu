@@ -1271,7 +1271,6 @@ lcma_status launch_simt(const lcma_plan_s* p, const float* A, const float* B, fl
 bool direct_ok(const lcma_plan_s* p) {
     if (p->variant != LCMA_VARIANT_FUSED_H || p->nbatch != 1 || p->d.b_layout != 1) return false;
     if (diag_env("LCMA_DEBUG") && (std::atoi(diag_env("LCMA_DEBUG")) & (16 | 32 | 64 | 4096))) return false;
-    if (diag_env("LCMA_OPERAND_HINT")) return false;
     if (diag_env("LCMA_DIRECT") && std::atoi(diag_env("LCMA_DIRECT")) == 0) return false;
     return true;
 }

@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef LCMA_DIAG
                         // diagnostics build: the general loop below whenever a knob
                         // changes what the producer issues
-                        const bool lean = !(p.debug & (16 | 32 | 64 | 4096)) && !p.operand_hint;
+                        const bool lean = !(p.debug & (16 | 32 | 64 | 4096));
 #else
                         constexpr bool lean = true;
 #endif
@@ -816,9 +816,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const uint32_t lbar = lbar0 + 8u * (uint32_t)stage;
                                 if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C_::kStageBytes * CG);
                                 const int kcol = kb * (F8 ? 128 : p.BK);
-                                ptx::tma_load_2d_cg2(sa, ma, lbar, ak0 + kcol, ar);
+                                ptx::tma_load_2d_cg2(sa, ma, lbar, ak0 + kcol, ar, ohint, opol);
                                 if (!p.b_mn_major)
-                                    ptx::tma_load_2d_cg2(sa + C_::kABytes, mb, lbar, bk0 + kcol, br);
+                                    ptx::tma_load_2d_cg2(sa + C_::kABytes, mb, lbar, bk0 + kcol, br, ohint, opol_b);
                                 else   // B stored K x N: one 3-D box {128 B, BK rows, BN/CG/BK chunks}
                                     ptx::tma_load_3d_cg2(sa + C_::kABytes, &tmap_b, lbar, 0, r * p.b_rows_per_r + kcol,
                                                          b_col0 / p.BK);
