@@ -86,6 +86,37 @@ for rnd in range(5):
         f, env, _ = runs[n]
         setenv(env)
         res[n].append(timed(f))
+# clock / power under sustained load per step (the paper's L2 thrash
+# lowered the H20's clock from 1.80 to 1.61 GHz): each arm runs back to back
+# for ~1 s while nvidia-smi samples SM clock and board power every 50 ms
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import ClockSampler
+import time
+power = {}
+for n in names:
+    f, env, _ = runs[n]
+    setenv(env)
+    f(); torch.cuda.synchronize()
+    smp = ClockSampler(torch.cuda.current_device())
+    smp.start()
+    time.sleep(0.2)
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        for _ in range(8):
+            f()
+        torch.cuda.synchronize()
+    smp.stop()
+    vals = []
+    for ln in smp.lines:
+        parts = [x.strip() for x in ln.split(",")]
+        try:
+            vals.append((float(parts[0]), float(parts[2])))
+        except (ValueError, IndexError):
+            pass
+    load = vals[len(vals) // 4:] or vals
+    power[n] = {"sm_mhz_median": statistics.median(v[0] for v in load) if load else None,
+                "power_w_median": statistics.median(v[1] for v in load) if load else None,
+                "samples": len(load)}
 setenv({})
 fl = 2.0 * M * N * K
 out = {"shape": [M, N, K], "algo": ALGO, "b_static": static, "b_layout": "NxK",
@@ -95,5 +126,5 @@ for n in names:
     info = runs[n][2]
     out["steps"][n] = {"ms": ms, "eff_tflops": fl / (ms * 1e-3) / 1e12,
                        "waves": info.get("waves"), "split_groups": info.get("split_groups"),
-                       "env": runs[n][1]}
+                       "env": runs[n][1], **power.get(n, {})}
 print(json.dumps(out, indent=1))
