@@ -1286,8 +1286,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __syncwarp();
                         if (lane == 0) {
                             const int brow0 = x * C_::kTileM + (int)rank * kBM + quarter * 32;
-                            ptx::tma_store_2d(&p.c_map, cst + cbuf * 2048, (int)ccol,
-                                              (int)((long long)i_blk * p.Mb + brow0 + radd));
+                            if (p.c_cs)   // C is never re-read here: evict-first in L2
+                                ptx::tma_store_2d_hint(&p.c_map, cst + cbuf * 2048, (int)ccol,
+                                                       (int)((long long)i_blk * p.Mb + brow0 + radd),
+                                                       ptx::policy_evict_first());
+                            else
+                                ptx::tma_store_2d(&p.c_map, cst + cbuf * 2048, (int)ccol,
+                                                  (int)((long long)i_blk * p.Mb + brow0 + radd));
                             ptx::bulk_commit_group();
                             ptx::bulk_wait_group_read<1>();
                         }
