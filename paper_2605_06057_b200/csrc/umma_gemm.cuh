@@ -1271,6 +1271,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // 16-bit C through shared memory and a TMA store: this lane's 16
                     // values at column half hh of the warp's current 32 x 32 box
                     auto c_stage16 = [&](int hh, const float* v) {
+                        if (p.c_tma == 2) {   // fp32 C: one 4 KB box (128-byte rows)
+                            const uint32_t dst = cst + lane * 128 + hh * 64;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                ptx::st_shared_v4(dst + 16 * q, __float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]),
+                                                  __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
+                            return;
+                        }
                         uint32_t wv[8];
 #pragma unroll
                         for (int h = 0; h < 8; ++h) wv[h] = pack2(p, v[2 * h], v[2 * h + 1]);
@@ -1286,7 +1294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __syncwarp();
                         if (lane == 0) {
                             const int brow0 = x * C_::kTileM + (int)rank * kBM + quarter * 32;
-                            if (p.c_cs)   // C is never re-read here: evict-first in L2
+                            if (p.c_cs && p.c_tma != 2)   // C is never re-read here: evict-first in L2
                                 ptx::tma_store_2d_hint(&p.c_map, cst + cbuf * 2048, (int)ccol,
                                                        (int)((long long)i_blk * p.Mb + brow0 + radd),
                                                        ptx::policy_evict_first());
@@ -1294,9 +1302,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::tma_store_2d(&p.c_map, cst + cbuf * 2048, (int)ccol,
                                                   (int)((long long)i_blk * p.Mb + brow0 + radd));
                             ptx::bulk_commit_group();
-                            ptx::bulk_wait_group_read<1>();
+                            // 16-bit: two boxes, the older store must have read its box;
+                            // fp32: one box, this store must have read it
+                            if (p.c_tma == 2) ptx::bulk_wait_group_read<0>();
+                            else ptx::bulk_wait_group_read<1>();
                         }
-                        cbuf ^= 1;
+                        if (p.c_tma != 2) cbuf ^= 1;
                         __syncwarp();
                     };
                     constexpr int ch = decltype(ch_c)::value;
