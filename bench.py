@@ -232,8 +232,9 @@ def _large_shape(L, inputs, torch, args):
 def _grid_corner(L, inputs, torch):
     """BASELINE cfg3's grid corner M=16384, N=K=14336 (paper layout, B K x N)
     in fp16 and tf32: the largest cfg3 shape, where the cfg3 sweep with the
-    final kernels measures Strassen ahead in fp16 (1.06x) and classical ahead
-    in tf32 (profiles/r02g_cfg3_decision.json); AUTO's choice beside both."""
+    final kernels measures Strassen ahead in fp16 (1.03x) and, with fp32 C
+    through TMA stores, in tf32 (1.09x in interleaved runs;
+    profiles/r02i_cfg3_decision.json); AUTO's choice beside both."""
     M, N, K = 16384, 14336, 14336
     out = {"shape": [M, N, K], "timing": "median of 5 interleaved rounds"}
     fl = 2.0 * M * N * K
