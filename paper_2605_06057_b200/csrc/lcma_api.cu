@@ -1062,6 +1062,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
             t_err.clear();
     }
     g.pf_kb = 0;
+    g.drift = 0;
+    if (const char* v = diag_env("LCMA_DRIFT")) g.drift = std::atoi(v);
     // in-place single-term operands (lean producer path only; the diagnostics
     // build takes the general loop when a producer knob is set)
     g.use_dir = 0;

@@ -162,7 +162,11 @@ struct GemmParams {
     int n_whole;           // groups processed whole before the split tail (static: q * W, <= G)
     int dyn;               // 1: whole groups handed out at run time in raster order (ticket
                            //    counter `sched`, broadcast to every role of the pair via a shared ring)
-    int* sched;            // dyn / dyn_tail: ticket counters [2] (workspace, zero between launches)
+    int* sched;            // dyn / dyn_tail: ticket counters [2] (workspace, zero between launches);
+                           // [2] lockstep progress (pairs x products started), [3] exit count
+    int drift;             // > 0: a pair starts product step s of the lockstep rounds only after
+                           // every pair started step s - drift (bounded drift: the round's operand
+                           // panels stay within the L2 window); 0: free-running
     int dyn_tail;          // 1: tail segments handed out at run time (DYN instantiation)
     int n_own;             // split groups of the tail (= owner segments)
     // batched GEMMs (two-level schemes: the R0 inner fused GEMMs of the outer
@@ -752,6 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool ohint = oh != 0;
             UnitIter<DYN> it(p, w, ring, leader ? SR_SCHED : SR_PEER, CG);
             Unit u;
+            int s_step = 0;          // lockstep product steps started (bounded-drift throttle)
             while (it.next(u, true)) {
                 int x, z;
                 group_xz(p, u.g, x, z);
@@ -780,6 +785,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int nk = p.nK;
                             [[maybe_unused]] const int ca0 = (a_row >> 7) * p.sf_nkb;
                             [[maybe_unused]] const int cb0 = ((r * p.b_rows_per_r + z * BN) >> 7) * p.sf_nkb;
+                            if (p.drift > 0 && leader && u.role == ROLE_WHOLE && p.sched) {
+                                // bounded drift: wait until every pair has started step
+                                // s - drift, then count this pair's start of step s
+                                const int target = (s_step - p.drift) * p.W;
+                                if (target > 0) {
+                                    int v;
+                                    do {
+                                        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.sched + 2) : "memory");
+                                    } while (v < target);
+                                }
+                                atomicAdd(p.sched + 2, 1);
+                                ++s_step;
+                            }
                             if (p.pf_kb > 0 && t + 1 < u.r1) {
                                 // product boundary: the next product's first k-blocks to L2
                                 // while this one streams (its panels are new to the round)
@@ -1636,6 +1654,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     ptx::tc_fence_before();
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+    if (p.drift > 0 && p.sched && threadIdx.x == 0) {
+        // the last CTA out resets the progress counter for the next launch
+        // (every producer of the grid has finished by then)
+        if (atomicAdd(p.sched + 3, 1) == (int)gridDim.x - 1) {
+            atomicExch(p.sched + 2, 0);
+            atomicExch(p.sched + 3, 0);
+        }
+    }
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<CG>(tmem_base, 512);
