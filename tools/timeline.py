@@ -11,9 +11,10 @@ from paper_2605_06057_b200 import inputs
 
 algo = sys.argv[1] if len(sys.argv) > 1 else "strassen"
 M, N, K = [int(v) for v in sys.argv[2:5]] if len(sys.argv) > 4 else (8192, 14336, 4096)
-A, B = inputs.operands(M, N, K, 0, 1, 2, b_layout=1)
+DT = int(os.environ.get("DT", "0"))
+A, B = inputs.operands(M, N, K, DT, 1, 2, b_layout=1)
 A, B = A.cuda(), B.cuda()
-p = L.Plan(M, N, K, algo=algo, b_layout=1, b_static=(algo != "classical"))
+p = L.Plan(M, N, K, dtype=DT, algo=algo, b_layout=1, b_static=(algo != "classical"))
 C = p.empty_c(); ws = p.workspace()
 Bt = p.precombine_b(B) if algo != "classical" else None
 f = (lambda: p.gemm_precombined(A, Bt, C, ws)) if Bt is not None else (lambda: p.gemm(A, B, C, ws))
@@ -42,3 +43,10 @@ for pos in range(R):
     e_ = epi[:, [k for k in ks]]
     print(f"  position {pos}: slot wait before it median {np.median(w_)/1e3:6.2f} us (p90 {np.percentile(w_,90)/1e3:6.2f}); "
           f"epilogue-to-release median {np.median(e_)/1e3:6.2f} us (p90 {np.percentile(e_,90)/1e3:6.2f})")
+# MMA issue time per product position and by round (where the mean exceeds the median)
+print("MMA issue time by position (us): " + "  ".join(
+    f"{pos}: p50 {np.median(prod[:, pos::R])/1e3:.2f} mean {np.mean(prod[:, pos::R])/1e3:.2f}" for pos in range(min(R, nprod))))
+nr = nprod // R
+if nr > 1:
+    per_round = [np.mean(prod[:, k * R:(k + 1) * R]) / 1e3 for k in range(nr)]
+    print("mean MMA issue per product by round (us):", " ".join(f"{v:.2f}" for v in per_round))
