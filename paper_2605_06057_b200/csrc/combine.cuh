@@ -115,12 +115,12 @@ __device__ __forceinline__ void store_vec(const CombineParams& p, long long off,
 // written with streaming (evict-first) stores.  Same arithmetic as below:
 // fp32 signed sum in coefficient order, one RN rounding.
 template <int PQ, int U>
-__global__ void __launch_bounds__(256, 4) group_combine16_kernel(const __grid_constant__ CombineParams p) {
+__device__ __forceinline__ void combine16_body(const CombineParams& p, int bid, int nblk) {
     const long long nvec = p.E0 * (p.E1 / 8);
     const long long per_r = p.E0 * p.E1;
-    const long long stride = (long long)gridDim.x * blockDim.x * U;
+    const long long stride = (long long)nblk * blockDim.x * U;
     const bool bf16 = p.elem == ELEM_BF16;
-    for (long long v0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * U; v0 < nvec; v0 += stride) {
+    for (long long v0 = (bid * (long long)blockDim.x + threadIdx.x) * U; v0 < nvec; v0 += stride) {
         uint4 src[U][PQ];
         long long e0s[U], e1s[U];
 #pragma unroll
@@ -180,6 +180,21 @@ __global__ void __launch_bounds__(256, 4) group_combine16_kernel(const __grid_co
             }
         }
     }
+}
+
+template <int PQ, int U>
+__global__ void __launch_bounds__(256, 4) group_combine16_kernel(const __grid_constant__ CombineParams p) {
+    combine16_body<PQ, U>(p, blockIdx.x, gridDim.x);
+}
+
+// Combine A and Combine B of one call in a single launch (blocks [0, nA)
+// take A, the rest B): one kernel boundary and one tail instead of two.
+template <int PQA, int PQB>
+__global__ void __launch_bounds__(256, 4) group_combine16_dual_kernel(const __grid_constant__ CombineParams pa,
+                                                                     const __grid_constant__ CombineParams pb,
+                                                                     int nA) {
+    if ((int)blockIdx.x < nA) combine16_body<PQA, 1>(pa, blockIdx.x, nA);
+    else combine16_body<PQB, 1>(pb, blockIdx.x - nA, gridDim.x - nA);
 }
 
 // Group Combine (Alg. 2 lines 2-9 / 11-18): out_r[e0][e1] =

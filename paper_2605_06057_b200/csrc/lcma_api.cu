@@ -785,10 +785,11 @@ int grid_for(long long work, int per_block) {
 }
 
 // Group combine of one operand into dst[R][E0][E1] (Alg. 2 stage 1 or 2).
-lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, bool is_b,
-                           cudaStream_t st, bool direct = false) {
+// Parameters of the group combine of one operand into dst[R][E0][E1]; inst =
+// the kernels' coefficient-table width (PQ instantiation).
+lcma_status make_combine_params(const lcma_plan_s* p, const void* src, void* dst, bool is_b, bool direct,
+                                CombineParams& c, int& inst) {
     const Scheme& S = p->sch;
-    CombineParams c;
     std::memset(&c, 0, sizeof(c));
     c.src = src;
     c.dst = dst;
@@ -808,7 +809,7 @@ lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, boo
     c.P = P;
     c.Q = Q;
     const int pq = P * Q;
-    const int inst = pq <= 4 ? 4 : pq <= 9 ? 9 : pq <= 16 ? 16 : pq <= 25 ? 25 : 32;
+    inst = pq <= 4 ? 4 : pq <= 9 ? 9 : pq <= 16 ? 16 : pq <= 25 ? 25 : 32;
     if (S.R > kCombMaxR || pq > kCombMaxPQ) return fail(LCMA_ERR_NOT_SUPPORTED, "scheme too large");
     for (int r = 0; r < S.R; ++r)
         for (int a = 0; a < P; ++a)
@@ -819,6 +820,39 @@ lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, boo
                 else v = S.v(r, b, a);
                 c.coef[r * inst + a * Q + b] = v;
             }
+    return LCMA_OK;
+}
+
+// Combine A and Combine B of one call (16-bit, packed kernels of the same
+// width) as one launch; otherwise two.
+lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, bool is_b, cudaStream_t st,
+                           bool direct = false);
+lcma_status launch_combine_ab(const lcma_plan_s* p, const void* A, void* At, const void* B, void* Bt,
+                              cudaStream_t st, bool dirA, bool dirB) {
+    CombineParams ca, cb;
+    int ia = 0, ib = 0;
+    lcma_status rs = make_combine_params(p, A, At, false, dirA, ca, ia);
+    if (rs == LCMA_OK) rs = make_combine_params(p, B, Bt, true, dirB, cb, ib);
+    if (rs != LCMA_OK) return rs;
+    if (ca.elem != ELEM_FP32 && ia == ib && (ia == 4 || ia == 9 || ia == 16) && !diag_env("LCMA_OLD_COMBINE") &&
+        !diag_env("LCMA_COMB_SPLIT")) {
+        const int ga = grid_for(ca.E0 * (ca.E1 / 8), 256), gb = grid_for(cb.E0 * (cb.E1 / 8), 256);
+        if (ia == 4) group_combine16_dual_kernel<4, 4><<<ga + gb, 256, 0, st>>>(ca, cb, ga);
+        else if (ia == 9) group_combine16_dual_kernel<9, 9><<<ga + gb, 256, 0, st>>>(ca, cb, ga);
+        else group_combine16_dual_kernel<16, 16><<<ga + gb, 256, 0, st>>>(ca, cb, ga);
+        return check_launch("group_combine16_dual_kernel");
+    }
+    rs = launch_combine(p, A, At, false, st, dirA);
+    if (rs != LCMA_OK) return rs;
+    return launch_combine(p, B, Bt, true, st, dirB);
+}
+
+lcma_status launch_combine(const lcma_plan_s* p, const void* src, void* dst, bool is_b,
+                           cudaStream_t st, bool direct) {   // (default: declaration above)
+    CombineParams c;
+    int inst = 0;
+    lcma_status rc = make_combine_params(p, src, dst, is_b, direct, c, inst);
+    if (rc != LCMA_OK) return rc;
     const bool fp32 = c.elem == ELEM_FP32;
     if (!fp32 && (inst == 4 || inst == 9 || inst == 16) && !diag_env("LCMA_OLD_COMBINE")) {
         // 16-bit sources with 9 or 16 blocks: packed sources keep more loads in
@@ -1336,7 +1370,12 @@ lcma_status run(lcma_plan_t p, const void* A, const void* B, const void* Bt_user
     const bool dir = direct_ok(p);
     const bool dirA = dir && p->any_a_dir;
     const bool dirB = dir && p->any_b_dir && !Bt_user && B;
-    if (p->variant != LCMA_VARIANT_PRODUCER) {
+    if (p->variant != LCMA_VARIANT_PRODUCER && !Bt_user) {
+        // Combine A (Eq. 3) and Combine B (Eq. 4) of this call in one launch
+        rs = launch_combine_ab(p, A, At, B, w + p->off_Bt, st, dirA, dirB);
+        if (rs != LCMA_OK) return rs;
+        Bt = w + p->off_Bt;
+    } else if (p->variant != LCMA_VARIANT_PRODUCER) {
         rs = launch_combine(p, A, At, false, st, dirA);            // Combine A (Eq. 3)
         if (rs != LCMA_OK) return rs;
     }
