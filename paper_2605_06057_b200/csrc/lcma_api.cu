@@ -1179,7 +1179,7 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     cfg.gridDim = dim3(p->ctas);
     cfg.blockDim = dim3(kThreads);
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     int na = 0;
     if (p->cg == 2) {
         attr[na].id = cudaLaunchAttributeClusterDimension;
@@ -1206,6 +1206,28 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         const size_t nb = std::min(region, (size_t)maxw);
         attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
         attr[na].val.accessPolicyWindow.base_ptr = P;
+        attr[na].val.accessPolicyWindow.num_bytes = nb;
+        attr[na].val.accessPolicyWindow.hitRatio = nb ? (float)std::min(1.0, (double)want / (double)nb) : 0.f;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
+    // diagnostics: a persisting access-policy window over the A operand
+    // (A~ panels are re-read by the lockstep rounds of a band)
+    if (!classical && !(P && g.epi_mode == EPI_FUSED && diag_env("LCMA_L2PERSIST")) && diag_env("LCMA_L2PERSIST_A")) {
+        size_t want = (size_t)std::atoll(diag_env("LCMA_L2PERSIST_A")) << 20;
+        int maxp = 0, maxw = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        want = std::min(want, (size_t)maxp);
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        const size_t region = (size_t)S.R * p->Mb * p->Kb * p->e;
+        const size_t nb = std::min(region, (size_t)maxw);
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = const_cast<void*>(Aop);
         attr[na].val.accessPolicyWindow.num_bytes = nb;
         attr[na].val.accessPolicyWindow.hitRatio = nb ? (float)std::min(1.0, (double)want / (double)nb) : 0.f;
         attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
