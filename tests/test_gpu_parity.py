@@ -449,3 +449,21 @@ def test_producer_fused_rejects():
     for args in ((1000, 512, 512, "strassen"), (512, 512, 520, "strassen"), (768, 768, 768, "laderman")):
         with pytest.raises(L.LcmaError):
             L.Plan(args[0], args[1], args[2], algo=args[3], variant="producer")
+
+
+@pytest.mark.parametrize("algo,shape", [("strassen", (1024, 1024, 512)), ("strassen", (2048, 1536, 1024)),
+                                        ("laderman", (768, 768, 384))])
+def test_inplace_single_term_operands_exact(algo, shape):
+    # exactly tiled shapes, B stored N x K: the single-term A~_r / B~_r are read
+    # in place from A / B (reading 25); per call and with B~ offline
+    # (A in place only), exact against the int64 oracle
+    M, N, K = shape
+    plan = _exact_case(M, N, K, algo, b_layout=1)
+    assert plan.info["Mb"] * (2 if algo == "strassen" else 3) == M
+    lo, hi = INT_RANGE[algo]
+    A, B = inputs.operands(M, N, K, 0, M + 7, N + K, dist="int", b_layout=1, lo=lo, hi=hi)
+    sp = L.Plan(M, N, K, dtype=0, algo=algo, out_dtype=L.FP32, b_layout=1, b_static=True)
+    Bt = sp.precombine_b(B.cuda())
+    C = sp.gemm_precombined(A.cuda(), Bt).cpu().numpy()
+    ref = O.gemm_i64(A.to(torch.int64).numpy(), B.t().to(torch.int64).numpy())
+    assert np.array_equal(C, ref)
