@@ -958,6 +958,10 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     int qf = 0;
     if (const char* v = diag_env("LCMA_QFULL"))
         qf = (!classical && !H && p->cg == 2 && p->bn == 256 && S.m * S.n > 1 && std::atoi(v) != 0) ? 1 : 0;
+    // diagnostics: the long-product register-home kernel without the shared
+    // partial home and with 7 operand stages
+    if (const char* v = diag_env("LCMA_NOSMEMP"))
+        if (std::atoi(v) != 0 && !classical && !H && p->cg == 2 && p->bn == 256 && p->nK > kCstMaxNK) qf = 2;
     // REGH: the instantiation with a register partial home (fused Combine H of
     // an LCMA scheme on 256-column pair tiles); classical / unfused GEMMs use
     // the one without (no 128 live registers reserved in the epilogue)
@@ -976,7 +980,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
                    : pf == 2 ? ensure_smem_attr<2, 256, 0, true, 2>()
                    : pf == 1 ? ensure_smem_attr<2, 256, 0, true, 1>()
                    : p->cg == 2 ? (p->bn == 128 ? ensure_smem_attr<2, 128>()
-                                                : (qf ? ensure_smem_attr<2, 256, 1, true>()
+                                                : (qf == 2 ? ensure_smem_attr<2, 256, 2, true>()
+                                                   : qf ? ensure_smem_attr<2, 256, 1, true>()
                                                       : regh ? (dyn ? (cst_regh ? ensure_smem_attr<2, 256, 0, true, 0, true>()
                                                                           : ensure_smem_attr<2, 256, 0, true, 0, true, false, false>())
                                                                     : cst_regh ? ensure_smem_attr<2, 256, 0, true>()
@@ -1152,7 +1157,8 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
         const int ns = po.nslot;
         const std::vector<int>& by_use = po.by_use;
         const bool use_reg = regh && !(diag_env("LCMA_REG_PARTIAL") && std::atoi(diag_env("LCMA_REG_PARTIAL")) == 0);
-        const bool use_smem = !H && !pf && !(diag_env("LCMA_SMEM_PARTIAL") && std::atoi(diag_env("LCMA_SMEM_PARTIAL")) == 0);
+        const bool use_smem = !H && !pf && qf != 2 &&
+                              !(diag_env("LCMA_SMEM_PARTIAL") && std::atoi(diag_env("LCMA_SMEM_PARTIAL")) == 0);
         std::vector<int> slot_home(ns, 0);
         int nl2 = 0, k0 = 0;
         if (use_reg && k0 < ns) slot_home[by_use[k0++]] = HOME_REG;
@@ -1277,6 +1283,9 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
             cfg.dynamicSmemBytes = Cfg<2, 256, 0, false, 1>::kSmemBytes;
             e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 0, true, 1>, ta, tb, g);
         }
+    } else if (p->cg == 2 && p->bn == 256 && qf == 2) {
+        cfg.dynamicSmemBytes = Cfg<2, 256, 2>::kSmemBytes;
+        e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 2, true>, ta, tb, g);
     } else if (p->cg == 2 && p->bn == 256 && qf) {
         cfg.dynamicSmemBytes = Cfg<2, 256, 1>::kSmemBytes;
         e = cudaLaunchKernelEx(&cfg, umma_gemm_kernel<2, 256, 1, true>, ta, tb, g);

@@ -88,10 +88,12 @@ struct Cfg {
         kABytes + kBBytes + (PF ? kABytes : 0) + (PF == 2 ? kBBytes : 0) + kSfBytes;   // PF: + staging
     // one C_ij partial kept in shared memory (fused Combine H, whole groups):
     // 128 rows x BN (QF) or BN/2 (column half 0) fp32
-    static constexpr int kPartialSmem = (NP || PF) ? 0 : kBM * (QF ? BN : BN / 2) * 4;
+    // QF = 2: no shared-memory partial home (all but the register slot in L2),
+    // the space goes to operand stages (long products)
+    static constexpr int kPartialSmem = (NP || PF || QF == 2) ? 0 : kBM * (QF ? BN : BN / 2) * 4;
     // F8: a 128-deep E4M3 k-block is half the MMA time of a 64-deep 16-bit one,
     // so the ring needs more stages to cover the same load latency
-    static constexpr int kMaxStages = F8 ? 8 : (NP ? LCMA_MAX_STAGES_NP : LCMA_MAX_STAGES);
+    static constexpr int kMaxStages = F8 ? 8 : (QF == 2 ? 7 : (NP ? LCMA_MAX_STAGES_NP : LCMA_MAX_STAGES));
     // as many stages as fit in 227 KB (minus the partial, alignment slack and
     // barriers), <= LCMA_MAX_STAGES
     // C staging for TMA stores of 16-bit C (GemmParams::c_tma): two 32 x 32
