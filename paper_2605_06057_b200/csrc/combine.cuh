@@ -265,25 +265,39 @@ __device__ __forceinline__ int ue8m0_exponent(float amax) {
     return e < -127 ? -127 : (e > 127 ? 127 : e);
 }
 
-template <int PQ>
+template <int PQ, int U>
 __global__ void __launch_bounds__(256) group_combine_q8_kernel(const __grid_constant__ CombineQ8Params p) {
     const long long nvec = p.E0 * (p.E1 / 8);
     const long long per_r = p.E0 * p.E1;
     const long long nkb = p.E1 / 128;
     const int lane = threadIdx.x & 31;
-    for (long long vi = blockIdx.x * (long long)blockDim.x + threadIdx.x; vi < nvec;
-         vi += (long long)gridDim.x * blockDim.x) {
+    // U vectors per thread, each from its own 256-vector chunk (16 consecutive
+    // lanes stay inside one 1 x 128 block): all U * PQ loads are issued before
+    // any arithmetic (memory-level parallelism)
+    uint4 srcs[U][PQ];
+    long long e0s[U], e1s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const long long vi = ((long long)blockIdx.x * U + u) * blockDim.x + threadIdx.x;
         const long long e0 = vi / (p.E1 / 8);
         const long long e1 = (vi - e0 * (p.E1 / 8)) * 8;
-        uint4 src[PQ];
+        e0s[u] = e0;
+        e1s[u] = e1;
 #pragma unroll
         for (int pq = 0; pq < PQ; ++pq) {
             const int pi = pq / p.Q, qi = pq - (pq / p.Q) * p.Q;
             const long long r = pi * p.E0 + e0, c = qi * p.E1 + e1;
-            src[pq] = (pq < p.P * p.Q && r < p.rows && c < p.cols)
-                          ? __ldcs(reinterpret_cast<const uint4*>(p.src + r * p.cols + c))
-                          : make_uint4(0, 0, 0, 0);
+            srcs[u][pq] = (vi < nvec && pq < p.P * p.Q && r < p.rows && c < p.cols)
+                              ? __ldcs(reinterpret_cast<const uint4*>(p.src + r * p.cols + c))
+                              : make_uint4(0, 0, 0, 0);
         }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const long long vi = ((long long)blockIdx.x * U + u) * blockDim.x + threadIdx.x;
+        if (vi >= nvec) break;                 // whole 256-vector chunks: uniform per warp
+        const long long e0 = e0s[u], e1 = e1s[u];
+        const uint4* src = srcs[u];
         for (int r = 0; r < p.R; ++r) {
             float acc[8];
 #pragma unroll
