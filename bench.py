@@ -205,7 +205,7 @@ def _large_shape(L, inputs, torch, args):
     M, N, K = 32768, 28672, 8192
     A, B = inputs.operands(M, N, K, L.BF16, 510, 502, b_layout=args.b_layout)
     A, B = A.cuda(), B.cuda()
-    out = {"shape": [M, N, K], "timing": "median of 9 interleaved rounds x 2 calls"}
+    out = {"shape": [M, N, K], "timing": "median of 15 interleaved rounds x 2 calls"}
     fl = 2.0 * M * N * K
     plans, fns = [], {}
     for name, kw in (("classical", dict(algo="classical")), ("strassen", dict(algo="strassen")),
@@ -219,7 +219,7 @@ def _large_shape(L, inputs, torch, args):
         else:
             fns[name] = (lambda p=p, C=C, ws=ws: p.gemm(A, B, C, ws))
         plans.append(p)
-    med = _interleaved(fns, 2, rounds=9)   # the 1 kW cap makes ratios drift: more rounds
+    med = _interleaved(fns, 2, rounds=15)   # the 1 kW cap makes ratios drift (+-5 %): more rounds
     for name, ms in med.items():
         out[name + "_tflops"] = fl / (ms * 1e-3) / 1e12
     out["strassen_vs_classical"] = out["strassen_tflops"] / out["classical_tflops"]
@@ -236,7 +236,7 @@ def _grid_corner(L, inputs, torch):
     through TMA stores, in tf32 (1.09x in interleaved runs;
     profiles/r02i_cfg3_decision.json); AUTO's choice beside both."""
     M, N, K = 16384, 14336, 14336
-    out = {"shape": [M, N, K], "timing": "median of 5 interleaved rounds"}
+    out = {"shape": [M, N, K], "timing": "median of 9 interleaved rounds"}
     fl = 2.0 * M * N * K
     for dt, name in ((L.FP16, "fp16"), (L.TF32, "tf32")):
         A, B = inputs.operands(M, N, K, dt, 301, 302)
@@ -247,7 +247,7 @@ def _grid_corner(L, inputs, torch):
             C, ws = p.empty_c(), p.workspace()
             fns[algo] = (lambda p=p, C=C, ws=ws: p.gemm(A, B, C, ws))
             keep += [p, C, ws]
-        med = _interleaved(fns, 1)
+        med = _interleaved(fns, 1, rounds=9)
         r = {"auto_choice": keep[6].info["scheme"]}
         for n, ms in med.items():
             r[n + "_tflops"] = fl / (ms * 1e-3) / 1e12
