@@ -1092,12 +1092,12 @@ lcma_status launch_umma(const lcma_plan_s* p, const void* Aop, const void* Bop, 
     const int ce = g.out_type == OUT_FP32 ? 4 : 2;
     if (has_stage && p->cg == 2 && !pf && !qf && !H && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
         (g.ldc * ce) % 16 == 0 && !(diag_env("LCMA_C_TMA") && std::atoi(diag_env("LCMA_C_TMA")) == 0)) {
-        // two 2 KB boxes per warp: 16-bit C 32 x 32, fp32 C (e.g. the
-        // two-level inner GEMMs' H_q) 32 rows x 16 columns
+        // 16-bit C: two 32 x 32 boxes per warp; fp32 C (e.g. the two-level
+        // inner GEMMs' H_q): one 32 x 32 box of 4 KB
         const CUtensorMapDataType ct = g.out_type == OUT_BF16   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                        : g.out_type == OUT_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                                 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-        if (make_map_t(&g.c_map, C, ct, ce, (uint64_t)p->d.N, (uint64_t)p->d.M * p->nbatch, ce == 4 ? 16 : 32, 32,
+        if (make_map_t(&g.c_map, C, ct, ce, (uint64_t)p->d.N, (uint64_t)p->d.M * p->nbatch, 32, 32,
                        CU_TENSOR_MAP_SWIZZLE_NONE) == LCMA_OK)
             g.c_tma = g.out_type == OUT_FP32 ? 2 : 1;
         else

@@ -1288,38 +1288,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // The chunk index is a template constant so that the register
                 // partial preg is indexed statically (stays in registers).
                 auto chunk = [=, &preg, &p, &cbuf](auto ch_c) {
-                    // C through shared memory and TMA stores.  One bulk store of the
-                    // warp's current 2 KB box (rows >= M, columns >= N clipped by the
-                    // map), then the other box; a box is reused once the store issued
-                    // before the current one has read it
-                    auto c_store_box = [&](int i_blk, long long col) {
-                        ptx::fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            const int brow0 = x * C_::kTileM + (int)rank * kBM + quarter * 32;
-                            const int grow = (int)((long long)i_blk * p.Mb + brow0 + radd);
-                            if (p.c_cs && p.c_tma != 2)   // C is never re-read here: evict-first in L2
-                                ptx::tma_store_2d_hint(&p.c_map, cst + cbuf * 2048, (int)col, grow,
-                                                       ptx::policy_evict_first());
-                            else
-                                ptx::tma_store_2d(&p.c_map, cst + cbuf * 2048, (int)col, grow);
-                            ptx::bulk_commit_group();
-                            ptx::bulk_wait_group_read<1>();
-                        }
-                        cbuf ^= 1;
-                        __syncwarp();
-                    };
-                    // this lane's 16 values at column half hh of the current chunk:
-                    // 16-bit C fills one 32 x 32 box per chunk (stored by c_flush),
-                    // fp32 C one 32 x 16 box per half, stored right away
-                    auto c_stage16 = [&](int hh, const float* v, int i_blk, long long ccol) {
-                        if (p.c_tma == 2) {
-                            const uint32_t dst = cst + cbuf * 2048 + lane * 64;
+                    // 16-bit C through shared memory and a TMA store: this lane's 16
+                    // values at column half hh of the warp's current 32 x 32 box
+                    auto c_stage16 = [&](int hh, const float* v) {
+                        if (p.c_tma == 2) {   // fp32 C: one 4 KB box (128-byte rows)
+                            const uint32_t dst = cst + lane * 128 + hh * 64;
 #pragma unroll
                             for (int q = 0; q < 4; ++q)
                                 ptx::st_shared_v4(dst + 16 * q, __float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]),
                                                   __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
-                            c_store_box(i_blk, ccol + 16 * hh);
                             return;
                         }
                         uint32_t wv[8];
@@ -1329,8 +1306,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::st_shared_v4(dst, wv[0], wv[1], wv[2], wv[3]);
                         ptx::st_shared_v4(dst + 16, wv[4], wv[5], wv[6], wv[7]);
                     };
+                    // the warp's box is complete: one bulk store (rows >= M, columns
+                    // >= N clipped by the map), then the other box; it is reused once
+                    // the store issued before this one has read it
                     auto c_flush = [&](int i_blk, long long ccol) {
-                        if (p.c_tma != 2) c_store_box(i_blk, ccol);
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int brow0 = x * C_::kTileM + (int)rank * kBM + quarter * 32;
+                            if (p.c_cs && p.c_tma != 2)   // C is never re-read here: evict-first in L2
+                                ptx::tma_store_2d_hint(&p.c_map, cst + cbuf * 2048, (int)ccol,
+                                                       (int)((long long)i_blk * p.Mb + brow0 + radd),
+                                                       ptx::policy_evict_first());
+                            else
+                                ptx::tma_store_2d(&p.c_map, cst + cbuf * 2048, (int)ccol,
+                                                  (int)((long long)i_blk * p.Mb + brow0 + radd));
+                            ptx::bulk_commit_group();
+                            // 16-bit: two boxes, the older store must have read its box;
+                            // fp32: one box, this store must have read it
+                            if (p.c_tma == 2) ptx::bulk_wait_group_read<0>();
+                            else ptx::bulk_wait_group_read<1>();
+                        }
+                        if (p.c_tma != 2) cbuf ^= 1;
+                        __syncwarp();
                     };
                     constexpr int ch = decltype(ch_c)::value;
                     uint32_t raw[32];
@@ -1390,8 +1388,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         pr[e] = (first ? 0.f : pr[e]) + sw * __uint_as_float(raw[e]);
                                     if (in_range && !(p.debug & 128)) {
                                         if (p.c_tma) {
-                                            c_stage16(0, pr, i, ccol);
-                                            c_stage16(1, pr + 16, i, ccol);
+                                            c_stage16(0, pr);
+                                            c_stage16(1, pr + 16);
                                             c_flush(i, ccol);
                                         } else {
                                             store_c_row16(p, (long long)i * p.Mb + brow, ccol, pr, radd);
@@ -1424,7 +1422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             v[e + 3] = o.w + sw * __uint_as_float(raw[hh + e + 3]);
                                         }
                                         if (in_range && !(p.debug & 128)) {
-                                            if (p.c_tma) c_stage16(hh >> 4, v, i, ccol);
+                                            if (p.c_tma) c_stage16(hh >> 4, v);
                                             else store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v, radd);
                                         }
                                     }
@@ -1465,7 +1463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             }
                                         }
                                         if (in_range && !(p.debug & 128)) {
-                                            if (p.c_tma) c_stage16(hh >> 4, v, i, ccol);
+                                            if (p.c_tma) c_stage16(hh >> 4, v);
                                             else store_c_row16(p, (long long)i * p.Mb + brow, ccol + hh, v, radd);
                                         }
                                     }
